@@ -1,0 +1,395 @@
+#!/usr/bin/env python
+"""bench.py -- initial-guess form+update throughput on B200 (arXiv 2009.10863 hot path).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    torchrun --nproc-per-node N --master-addr 127.0.0.1 ... bench.py --gpus N ...
+
+Workload (BASELINE.json configs[1], "C2"): 3D 128^3 7-point Helmholtz manufactured sequence
+(2,097,152 fp64 DOFs per GPU), projection QR(8) and extrapolation EXTRAP(3,8) on the same
+time steps.  One STEP = the whole hot path once: QR form + QR update + EXTRAP form + EXTRAP
+update (push by copy) on that step's fresh (b_n, x_n, A x_n), all resident in HBM.
+With N > 1 every rank holds a contiguous z-slab of 128^3 DOFs of a 128x128x(128N) global
+problem (weak scaling); the projection's global sums go over NCCL, extrapolation never
+communicates.
+
+value = effective HBM GB/s of the whole job = (algorithmic bytes of all ranks) / (max-over-ranks
+device time), algorithmic bytes per step and rank = [(8M+4) + (M+1) + 2] * 8 * N (DESIGN.md
+"Bytes").  ms_per_step is reported beside it.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "initial-guess form+update time/step & effective HBM GB/s (% of roofline), 1/2/4/8 B200"
+FALLBACK_HBM = 6650.0  # B200_PROFILING.md fallback (GB/s)
+L2_BYTES = 126 * 2 ** 20
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=200)
+    p.add_argument("--warmup", type=int, default=10)
+    p.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    p.add_argument("--n", type=int, default=128, help="grid points per direction (per-GPU slab n^3)")
+    p.add_argument("--m", type=int, default=8, help="history size M (projection and extrapolation)")
+    p.add_argument("--degree", type=int, default=3, help="extrapolation degree")
+    p.add_argument("--e2e-steps", type=int, default=20)
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--cpu-seconds", type=float, default=15.0, help="budget of the oracle cpu_baseline sample")
+    return p.parse_args()
+
+
+def peak_hbm():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy read+write)"
+    except Exception:
+        return FALLBACK_HBM, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def bytes_per_step(M: int, N: int):
+    """Algorithmic fp64 traffic of one steady step."""
+    vb = 8 * N
+    proj = (8 * M + 4) * vb  # form 2(M+1) + U1 2M + U2 M + U3 3M+2
+    extrap = (M + 1) * vb + 2 * vb  # combine of M + write x0, push by copy
+    per_kernel = {"form_dot": (M + 1) * vb, "form_combine": (M + 1) * vb, "u1": 2 * M * vb, "u2": M * vb,
+                  "u3": (3 * M + 2) * vb, "extrap": (M + 1) * vb, "copy": 2 * vb}
+    return proj, extrap, per_kernel
+
+
+class ClockSampler:
+    """Samples SM clock and throttle reasons with NVML during the timed region."""
+
+    REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+               0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+               0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting"}
+
+    def __init__(self, dev_index: int):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self._stop = threading.Event()
+        self.ok = False
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(dev_index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception as e:  # pragma: no cover
+            self.err = str(e)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if r & bit and name != "gpu_idle":
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(0.002)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.ok:
+            self._stop.set()
+            self.t.join()
+
+    def summary(self):
+        if not self.ok or not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons), "samples": 0}
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+def dist_setup(args):
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.gpus != world and world > 1:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    if torch.cuda.is_available():
+        torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl" if torch.cuda.is_available() else "gloo")
+    return world, rank, local
+
+
+def max_over_ranks(v: float, world: int) -> float:
+    if world == 1:
+        return v
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([v], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(world: int):
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+
+
+# ------------------------------------------------------------------------------------------ oracle arm
+def oracle_sample_run(n: int, M: int, degree: int, nz: int, steps: int, budget_s: float | None, fill: int):
+    """Time the CPU oracle (as it stands) on a contiguous z-slab sample of the C2 grid.
+
+    Returns (seconds per step, bytes per step, steps timed, N_sample)."""
+    import numpy as np
+
+    from oracle import ExtrapLS, ProjQR
+    from workloads.gen import manufactured_step_slab
+
+    world_equiv = n // nz
+    N = n * n * nz
+    op, oe = ProjQR(N, M), ExtrapLS(N, M, degree)
+
+    def gen(k):
+        return tuple(t.numpy() for t in manufactured_step_slab(n, nz, 0, world_equiv, k))
+
+    x_prev = np.zeros(N)
+    for k in range(fill):  # history fill, untimed
+        b, x, Ax = gen(k)
+        op.form_guess(b, x_prev)
+        op.update(x, Ax)
+        oe.form_guess(b, x_prev)
+        oe.update(x)
+        x_prev = x
+    tot, done = 0.0, 0
+    k = fill
+    while done < steps and (budget_s is None or tot < budget_s):
+        b, x, Ax = gen(k)
+        t0 = time.perf_counter()
+        op.form_guess(b, x_prev)
+        op.update(x, Ax)
+        oe.form_guess(b, x_prev)
+        oe.update(x)
+        tot += time.perf_counter() - t0
+        x_prev = x
+        done += 1
+        k += 1
+    pb, eb, _ = bytes_per_step(M, N)
+    return tot / max(done, 1), pb + eb, done, N
+
+
+def cpu_cores():
+    try:
+        from threadpoolctl import threadpool_info
+
+        th = [i.get("num_threads", 0) for i in threadpool_info() if i.get("user_api") == "blas"]
+        if th:
+            return max(th)
+    except Exception:
+        pass
+    return os.cpu_count()
+
+
+def run_reference(args, world, rank):
+    """--impl reference: the oracle timed on the host cores (rank 0 only)."""
+    if rank != 0:
+        return
+    n, M, p = args.n, args.m, args.degree
+    nz = max(1, n // 8)
+    # warm-up steps double as history fill; each timed step is one oracle step on the sample
+    sps, bps, done, Ns = oracle_sample_run(n, M, p, nz, args.steps, None, max(args.warmup, M + 1))
+    gbs = bps / sps / 1e9
+    sample = (f"{nz} of {n} z-planes of the {n}^3 C2 grid ({Ns} DOFs), QR({M}) + EXTRAP({p},{M}) oracle steps, "
+              f"{done} timed after {max(args.warmup, M + 1)} fill steps")
+    out = {"metric": METRIC, "value": gbs, "unit": "GB/s", "n_gpus": args.gpus, "steps": args.steps,
+           "warmup": args.warmup, "ms_per_step": sps * 1e3 * (n // nz), "higher_is_better": True,
+           "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
+           "config": {"workload": f"C2 3D {n}^3 7-point Helmholtz manufactured sequence, QR({M}) + EXTRAP({p},{M})",
+                      "sample": sample, "ms_per_step_note": "sample time scaled to the full grid"},
+           "cpu_baseline": {"value": gbs, "unit": "GB/s", "cores": cpu_cores(), "kind": "oracle", "sample": sample},
+           "e2e": {"value": gbs, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
+# ------------------------------------------------------------------------------------------ our arm
+def run_ours(args, world, rank, local):
+    import torch
+
+    from paper_2009_10863_b200 import (InitialGuess, comm_from_process_group, ig_form_guess_host, ig_profile,
+                                       ig_profile_read, ig_total_launches, ig_update_host)
+    from workloads.gen import manufactured_step_slab
+
+    n, M, p = args.n, args.m, args.degree
+    N = n * n * n
+    K, W = args.steps, args.warmup
+    prefill = max(0, M + 1 - W)  # untimed history fill when W is too short to reach the steady state
+    S = prefill + W + K
+    dev = torch.device("cuda", local)
+
+    # ---- inputs resident in HBM before the timed region: one fresh (b, x, Ax) per step
+    pool = [manufactured_step_slab(n, n, rank, world, k, device=dev) for k in range(S)]
+    torch.cuda.synchronize()
+
+    comm = comm_from_process_group() if world > 1 else None
+    hp = InitialGuess(N, "proj_qr", M, comm=comm)
+    he = InitialGuess(N, "extrap_ls", M, p)
+    x0p = torch.zeros(N, dtype=torch.float64, device=dev)
+    x0e = torch.zeros(N, dtype=torch.float64, device=dev)
+
+    def step(k):
+        b, x, Ax = pool[k % S]
+        hp.form_guess(b, x0p)
+        hp.update(x, Ax)
+        he.form_guess(None, x0e)
+        he.update(x)
+
+    for k in range(prefill + W):
+        step(k)
+    torch.cuda.synchronize()
+    assert hp.d == M, f"projection history not full after warm-up (d={hp.d})"
+
+    stream = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    sampler = ClockSampler(local)
+    barrier(world)
+    torch.cuda.synchronize()
+    l0 = ig_total_launches()
+    with sampler:
+        e0.record(stream)
+        for k in range(prefill + W, S):
+            step(k)
+        e1.record(stream)
+        torch.cuda.synchronize()
+    barrier(world)
+    launches = ig_total_launches() - l0
+    t_ms = max_over_ranks(e0.elapsed_time(e1), world)
+    st = hp.stats()
+    fb, ub = hp.bytes()
+    pb, eb, per_kernel = bytes_per_step(M, N)
+    assert fb + ub == pb, f"library byte count {fb + ub} != analytic {pb}"
+    assert st["admitted"] == 1
+
+    step_bytes = pb + eb
+    value = world * step_bytes * K / (t_ms * 1e-3) / 1e9
+    ms_per_step = t_ms / K
+
+    # ---- per-kernel CUDA-event timing over a second K-step pass (same inputs, cycled)
+    ig_profile(hp.h, True)
+    ig_profile(he.h, True)
+    for k in range(prefill + W, S):
+        step(k)
+    torch.cuda.synchronize()
+    prof = ig_profile_read(hp.h)
+    prof_e = ig_profile_read(he.h)
+    for kk in ("extrap", "copy"):
+        prof[kk] = prof_e[kk]
+    ig_profile(hp.h, False)
+    ig_profile(he.h, False)
+    kernels = {}
+    step_kernel_ms = sum(v[0] for v in prof.values()) / K
+    for name, (ms, cnt) in prof.items():
+        if cnt:
+            avg = ms / cnt
+            kernels[name] = {"avg_us": avg * 1e3, "launches": cnt, "gbs": per_kernel[name] / (avg * 1e-3) / 1e9,
+                             "share": (ms / K) / step_kernel_ms}
+    dom = max(kernels, key=lambda k: kernels[k]["avg_us"] * kernels[k]["launches"])
+    peak, peak_src = peak_hbm()
+    traffic, traffic_src = None, None
+    tpath = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tpath):
+        try:
+            with open(tpath) as f:
+                tj = json.load(f)
+            key = f"{dom}@M{M}N{N}"
+            if key in tj:
+                traffic, traffic_src = tj[key], "profiles/traffic.json (ncu --set full dram__bytes_read+write)"
+        except Exception:
+            pass
+    roofline = {"bound": "hbm", "kernel": f"k_{dom}", "achieved": kernels[dom]["gbs"], "peak": peak, "unit": "GB/s",
+                "frac": kernels[dom]["gbs"] / peak, "traffic": traffic, "peak_source": peak_src,
+                "algorithmic_bytes_per_launch": per_kernel[dom], "traffic_source": traffic_src,
+                "step_frac": (step_bytes / (ms_per_step * 1e-3) / 1e9) / peak}
+
+    # ---- end to end through the public host-buffer API (H2D of inputs and D2H of guesses timed)
+    P = min(4, S)
+    host = [tuple(t.cpu().pin_memory() for t in pool[prefill + W + j]) for j in range(P)]
+    x0h_p = torch.zeros(N, dtype=torch.float64).pin_memory()
+    x0h_e = torch.zeros(N, dtype=torch.float64).pin_memory()
+    KE = max(1, args.e2e_steps)
+    barrier(world)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for j in range(KE):
+        b, x, Ax = host[j % P]
+        ig_form_guess_host(hp.h, b, x0h_p)
+        ig_update_host(hp.h, x, Ax)
+        ig_form_guess_host(he.h, None, x0h_e)
+        ig_update_host(he.h, x, None)
+    torch.cuda.synchronize()
+    te = max_over_ranks(time.perf_counter() - t0, world)
+    e2e = {"value": world * step_bytes * KE / te / 1e9, "unit": "GB/s", "ms_per_step": te / KE * 1e3,
+           "h2d_bytes_per_step": 5 * 8 * N, "d2h_bytes_per_step": 2 * 8 * N, "steps": KE,
+           "api": "ig_form_guess_host/ig_update_host (pinned host buffers)"}
+
+    # ---- CPU oracle baseline (rank 0, N=1 only)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        sps, bps, done, Ns = oracle_sample_run(n, M, p, n, 10 ** 6, args.cpu_seconds, M + 1)
+        cpu = {"value": bps / sps / 1e9, "unit": "GB/s", "cores": cpu_cores(), "kind": "oracle",
+               "ms_per_step": sps * 1e3,
+               "sample": f"full {n}^3 grid ({Ns} DOFs), {done} steady oracle steps (QR({M})+EXTRAP({p},{M})) "
+                         f"after {M + 1} fill steps, ~{args.cpu_seconds:.0f} s budget"}
+
+    hp.close()
+    he.close()
+    if rank == 0:
+        out = {"metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": K, "warmup": W,
+               "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+               "dtype": "f64", "data": "synthetic",
+               "config": {"workload": f"C2 3D {n}^3 7-point Helmholtz manufactured sequence, QR({M}) + EXTRAP({p},{M})",
+                          "dofs_per_gpu": N, "history_m": M, "degree": p, "prefill_steps": prefill,
+                          "bytes_per_step_per_gpu": step_bytes,
+                          "bytes_model": "QR (8M+4)*8N + EXTRAP (M+1)*8N + push copy 2*8N",
+                          "l2": f"fresh inputs every step; per-step working set "
+                                f"{(2 * M + M + 5) * 8 * N / 1e9:.2f} GB > L2 126 MB",
+                          "parallelism": f"dof-shard{world}" if world > 1 else "single"},
+               "gpu_launches": launches, "roofline": roofline, "kernels": kernels,
+               "clocks": sampler.summary(), "e2e": e2e, "cpu_baseline": cpu,
+               "proj_state": {"d": st["d"], "rho_last": st["rho"]}}
+        print(json.dumps(out), flush=True)
+
+
+def main():
+    args = parse()
+    world, rank, local = dist_setup(args)
+    if args.impl == "reference":
+        run_reference(args, world, rank)
+    else:
+        run_ours(args, world, rank, local)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,186 @@
+/*
+ * ig.h -- C ABI of libig.so: B200 (sm_100a) initial guesses for sequences of linear systems
+ *         A x_n = b_n, after arXiv 2009.10863 ("PAPER.md" below = /root/reference/PAPER.md).
+ *
+ * Methods (all fp64):
+ *   IG_PROJ_QR       Fischer right-hand-side projection with rolling-QR history updates,
+ *                    Algorithm 2 "Rolling QR" (§2).  QR(M).
+ *   IG_EXTRAP_LS     Stabilized least-squares polynomial extrapolation, Eq. EXTRAPEXPN
+ *                     with weights Eq. LSQRCOEFFS (§3.2).
+ *                    EXTRAP(degree, M).
+ *   IG_PROJ_CLASSIC  Algorithm 1 "Classic": restart when d >= M.  CLASSIC(M).
+ *   IG_EXTRAP_SPARSE Sparse (column-pivoted QR) extrapolation, Eq. CPQRCOEFFS (§3.3).
+ *
+ * Conventions (every function):
+ *   - Vectors are DEVICE pointers to fp64[N] (N = this rank's local length), caller-owned,
+ *     unless the name ends in _host (then pinned or pageable HOST pointers).
+ *   - Calls enqueue work on the handle's CUDA stream and return without synchronising, except
+ *     where stated ("syncs").  Asynchronous CUDA faults surface as IG_E_CUDA at a later call.
+ *   - History storage (B~, X~, the solution ring, R) is owned by the library.
+ *   - Return value: IG_OK (0) or an ig_status code; ig_last_error() gives a thread-local message.
+ *   - A handle is used by one host thread at a time.  Handles are independent (one per field,
+ *     PAPER.md:903-907).
+ *   - Multi-GPU: every rank calls the same sequence with its contiguous DOF slice; after
+ *     ig_attach_comm the projection's global sums are exchanged with NCCL (all-gather of the
+ *     per-rank partial sums, summed in rank order: bitwise-identical decisions on all ranks).
+ *     Extrapolation never communicates.
+ */
+#ifndef IG_H
+#define IG_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define IG_MAX_HISTORY 32 /* M <= 32 */
+
+typedef struct ig_ctx *ig_t;
+typedef struct ig_comm_ctx *ig_comm_t;
+
+enum ig_method {
+    IG_PROJ_QR = 1,
+    IG_EXTRAP_LS = 2,
+    IG_PROJ_CLASSIC = 3,
+    IG_EXTRAP_SPARSE = 4
+};
+
+enum ig_status {
+    IG_OK = 0,
+    IG_E_ARG = 1,   /* invalid argument (sizes, method, NULL pointer, misuse)              */
+    IG_E_OOM = 2,   /* device allocation failed                                           */
+    IG_E_CUDA = 3,  /* CUDA runtime error (also asynchronous faults of earlier calls)      */
+    IG_E_NCCL = 4,  /* NCCL could not be loaded or a collective failed                     */
+    IG_E_STATE = 5  /* call not valid in the handle's current state                       */
+};
+
+/* ---------------------------------------------------------------- lifecycle */
+
+/* Create a handle for vectors of local length N.
+ *   method : enum ig_method.
+ *   m      : history capacity M (paper's M; BASELINE "m"), 1 <= m <= IG_MAX_HISTORY.
+ *   degree : extrapolation degree (paper's m); 0 <= degree <= m-1 (M >= m+1).
+ *            Ignored for the projection methods.
+ * Allocates the history slabs on the current CUDA device: projection 2*m*N doubles (B~, X~,
+ * PAPER.md:310-315), extrapolation m*N doubles (the solution window).  Extrapolation weights
+ * (incl. the warm-up table for f < M stored solutions) are built here, on the host, once.
+ * Returns NULL on error (see ig_last_error()). */
+ig_t ig_create(int64_t N, int method, int m, int degree);
+
+/* As ig_create, but the history slabs live in caller-provided device memory `storage` of
+ * `bytes` >= ig_storage_bytes(N, method, m) bytes, 256-byte aligned (e.g. a torch tensor). */
+ig_t ig_create_ext(int64_t N, int method, int m, int degree, void *storage, size_t bytes);
+size_t ig_storage_bytes(int64_t N, int method, int m);
+
+/* Release the handle (syncs its stream first).  NULL is a no-op. */
+void ig_destroy(ig_t h);
+
+/* Forget all history (d = 0 / empty window).  Enqueued on the stream. */
+int ig_reset(ig_t h);
+
+const char *ig_last_error(void);
+
+/* Stream all subsequent work of h is enqueued on (a cudaStream_t; NULL = legacy default). */
+int ig_set_stream(ig_t h, void *cuda_stream);
+
+/* Projection admission tolerance (AMB-3 reading of PAPER.md:209-215, 246, 302): the new pair is
+ * admitted iff ||b~|| > eps_rel * ||A x|| after the two Gram-Schmidt passes.  Default 1e-10. */
+int ig_set_admit_tol(ig_t h, double eps_rel);
+
+/* ---------------------------------------------------------------- the hot path */
+
+/* Form the initial guess for A x = b.
+ *   Projection (Alg. 2 line 1): if d > 0, x0 <- X~ (B~_{:,1:d}^T b); if d == 0,
+ *     x0 is left untouched (it is the caller's "arbitrary input").
+ *   Extrapolation (Eq. EXTRAPEXPN): x0 <- sum_i beta_i x_{n-f+i} over the f = min(fill, M) stored
+ *     solutions, oldest first; fill == 0 leaves x0 untouched.  b is ignored (may be NULL).
+ * x0 may alias b.  x0 may alias ig_next_slot(h) (extrapolation).  Neither may alias other
+ * history storage. */
+int ig_form_guess(ig_t h, const double *b, double *x0);
+
+/* Update the history with the solution x of the system just solved.
+ *   Projection (Alg. 2 after the solve): Ax must be A*x (an explicit operator
+ *     apply).  If d == M the oldest pair is dropped by a Givens QR downdate; then
+ *     (x, Ax) is orthogonalised by twice-iterated classical Gram-Schmidt and admitted iff
+ *     ||b~|| > eps*||Ax|| (d == 0: admitted iff ||Ax|| > 0).
+ *   Extrapolation: x is pushed into the solution window (Ax ignored, may be NULL).  If
+ *     x == ig_next_slot(h) nothing is copied; otherwise one copy. */
+int ig_update(ig_t h, const double *x, const double *Ax);
+
+/* Host-buffer variants (end-to-end path): inputs are copied host->device into handle-owned
+ * staging buffers on the stream, the result device->host; these SYNC before returning.
+ *   ig_form_guess_host: x0 (in: fallback, out: guess) and b are host arrays of N doubles.
+ *   ig_update_host    : x, Ax host arrays (Ax may be NULL for extrapolation). */
+int ig_form_guess_host(ig_t h, const double *b, double *x0);
+int ig_update_host(ig_t h, const double *x, const double *Ax);
+
+/* Extrapolation zero-copy slot: the device vector the next ig_update(h, slot, NULL) will push
+ * without a copy.  The caller may solve directly into it (it may also be the x0 of
+ * ig_form_guess).  NULL for projection methods. */
+double *ig_next_slot(ig_t h);
+
+/* ---------------------------------------------------------------- multi-GPU */
+
+/* Write a fresh NCCL unique id (128 bytes) into out (call on one rank, broadcast the bytes). */
+int ig_comm_unique_id(void *out128);
+/* Create a communicator over nranks processes (one GPU each; current device).  NCCL is loaded
+ * at run time (dlopen "libnccl.so.2"); IG_E_NCCL if unavailable. */
+int ig_comm_create(int nranks, int rank, const void *id128, ig_comm_t *out);
+void ig_comm_destroy(ig_comm_t c);
+/* Attach a communicator to a handle (projection: global sums over all ranks).  The handle's
+ * N is then the LOCAL slice length; ranks may have different N. */
+int ig_attach_comm(ig_t h, ig_comm_t c);
+
+/* ---------------------------------------------------------------- introspection (tests/bench) */
+
+/* Current history dimension d (projection) or fill (extrapolation).  Syncs. */
+int ig_history_dim(ig_t h, int *d);
+
+/* Extrapolation: the weights used with f stored solutions (1 <= f <= M), oldest first;
+ * *len receives f.  f == 0 means the steady-state scheme (f = M). */
+int ig_weights(ig_t h, int f, double *beta, int *len);
+
+/* Algorithmic bytes (8 bytes per fp64 value loaded or stored) of the last ig_form_guess and
+ * the last ig_update, per the fused schedule in DESIGN.md "Bytes".  Syncs (reads d). */
+int ig_bytes(ig_t h, int64_t *form_bytes, int64_t *update_bytes);
+
+typedef struct ig_stats {
+    int d;            /* history dimension / fill after the last call                     */
+    int admitted;     /* projection: last update admitted its pair (1) or not (0)         */
+    double rho;       /* projection: ||b~||/||A x|| of the last update                    */
+    double norm_Ax;   /* projection: ||A x|| of the last update                            */
+    double norm_bt;   /* projection: ||b~|| after the two Gram-Schmidt passes              */
+    int64_t launches; /* kernels this handle has launched since creation                   */
+} ig_stats_t;
+int ig_get_stats(ig_t h, ig_stats_t *out); /* syncs */
+
+/* Copy the projection state out (syncs).  Bt_dst/Xt_dst: DEVICE buffers of m columns of length
+ * ld_dst (column k at +k*ld_dst); R_host: HOST m*m, column-major.  Any pointer may be NULL. */
+int ig_copy_history(ig_t h, double *Bt_dst, double *Xt_dst, int64_t ld_dst, double *R_host);
+
+/* Number of CUDA kernels launched by this process through libig (all handles). */
+int64_t ig_total_launches(void);
+
+/* Per-kernel timing with CUDA events recorded on the handle's stream around every launch
+ * (tracing aid for bench.py's roofline; off by default).  ig_profile(h, 1) clears the counters
+ * and turns it on, ig_profile(h, 0) turns it off.  ig_profile_read syncs and returns the summed
+ * event time and launch count of one kernel since the last ig_profile call. */
+enum ig_kernel {
+    IG_K_FORM_DOT = 0,     /* alpha = B~^T b            (paper: rhsProject)               */
+    IG_K_FORM_COMBINE = 1, /* x0 = X~ alpha             (paper: rhsReconstruct)           */
+    IG_K_U1 = 2,           /* B~ Givens downdate + c1   (paper: rhsQRUpdate + rhsProject) */
+    IG_K_U2 = 3,           /* CGS pass 2 dots           (paper: rhsReconstruct+rhsProject)*/
+    IG_K_U3 = 4,           /* X~ downdate + store       (paper: rhsUpdateSpace, ...)      */
+    IG_K_EXTRAP = 5,       /* x0 = sum beta_i x_i       (paper: extrapKernel)             */
+    IG_K_COPY = 6,         /* window push by copy                                        */
+    IG_NKERNELS = 7
+};
+int ig_profile(ig_t h, int enable);
+int ig_profile_read(ig_t h, int kernel, double *total_ms, int64_t *launches);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* IG_H */

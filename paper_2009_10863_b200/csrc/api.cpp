@@ -1,0 +1,655 @@
+// api.cpp -- libig C ABI (include/ig.h): handles, history storage, stream-ordered launch
+// sequence of the hot path, NCCL exchange of the projection's partial sums, host staging.
+//
+// Per-step launch sequence (all asynchronous on the handle's stream, no host sync):
+//   PROJ  form   : k_form_dot -> [all-gather alpha partials] -> k_form_combine
+//         update : k_u1 -> [all-gather] -> k_u2 -> [all-gather] -> k_u3
+//   EXTRAP form  : k_extrap (weights + slot pointers by value)
+//          update: ring bump (0 bytes) or k_copy
+#include <dlfcn.h>
+
+#include <atomic>
+#include <cstdarg>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "ig.h"
+#include "ig_internal.h"
+
+using namespace ig;
+
+static thread_local std::string g_err;
+static std::atomic<int64_t> g_launches{0};
+
+static int set_err(int code, const char *fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return code;
+}
+
+#define CUDA_OK(expr)                                                                          \
+    do {                                                                                       \
+        cudaError_t e_ = (expr);                                                               \
+        if (e_ != cudaSuccess)                                                                 \
+            return set_err(IG_E_CUDA, "%s: %s (%s:%d)", #expr, cudaGetErrorString(e_), __FILE__, __LINE__); \
+    } while (0)
+
+// ----------------------------------------------------------------------------- NCCL (dlopen)
+namespace {
+typedef int ncclResult_t;
+typedef void *ncclComm_t;
+struct ncclUniqueId {
+    char internal[128];
+};
+const int ncclFloat64 = 8;  // nccl.h: ncclFloat64 = 8
+
+struct NcclApi {
+    bool ok = false;
+    std::string why;
+    ncclResult_t (*getUniqueId)(ncclUniqueId *) = nullptr;
+    ncclResult_t (*commInitRank)(ncclComm_t *, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*allGather)(const void *, void *, size_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
+    const char *(*errStr)(ncclResult_t) = nullptr;
+};
+
+NcclApi &nccl() {
+    static NcclApi api;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        const char *env = getenv("IG_NCCL_PATH");
+        void *lib = nullptr;
+        if (env && *env) lib = dlopen(env, RTLD_NOW | RTLD_GLOBAL);
+        if (!lib) lib = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (!lib) {
+            api.why = std::string("dlopen libnccl.so.2 failed: ") + dlerror();
+            return;
+        }
+        api.getUniqueId = (decltype(api.getUniqueId))dlsym(lib, "ncclGetUniqueId");
+        api.commInitRank = (decltype(api.commInitRank))dlsym(lib, "ncclCommInitRank");
+        api.allGather = (decltype(api.allGather))dlsym(lib, "ncclAllGather");
+        api.commDestroy = (decltype(api.commDestroy))dlsym(lib, "ncclCommDestroy");
+        api.errStr = (decltype(api.errStr))dlsym(lib, "ncclGetErrorString");
+        api.ok = api.getUniqueId && api.commInitRank && api.allGather && api.commDestroy && api.errStr;
+        if (!api.ok) api.why = "libnccl.so.2 lacks required symbols";
+    });
+    return api;
+}
+}  // namespace
+
+struct ig_comm_ctx {
+    ncclComm_t comm = nullptr;
+    int nranks = 1, rank = 0;
+};
+
+// ----------------------------------------------------------------------------- handle
+struct ig_ctx {
+    int64_t N = 0, ld = 0;
+    int method = 0, M = 0, degree = 0;
+    double eps = 1e-10;
+    cudaStream_t stream = nullptr;
+    int dev = 0, nsm = 148;
+    double *slab = nullptr;
+    size_t slab_bytes = 0;
+    bool own_slab = false;
+    // projection
+    double *Bt = nullptr, *Xt = nullptr;
+    Ctrl *ctrl = nullptr;
+    double *blk = nullptr, *part = nullptr, *gath = nullptr;
+    int G = 1;
+    ig_comm_ctx *comm = nullptr;
+    // extrapolation
+    std::vector<std::vector<double>> table;  // table[f-1]: weights for f stored solutions
+    std::vector<double *> slots;
+    int head = 0, fill = 0;
+    bool last_copy = false;
+    int last_form_f = 0;
+    // host staging (end-to-end path)
+    double *stage[4] = {nullptr, nullptr, nullptr, nullptr};
+    int64_t launches = 0;
+    // per-kernel CUDA-event timing (ig_profile)
+    bool profiling = false;
+    std::vector<cudaEvent_t> ev_pool;
+    struct Rec { int kid; cudaEvent_t a, b; };
+    std::vector<Rec> recs;
+    double prof_ms[IG_NKERNELS] = {0};
+    int64_t prof_n[IG_NKERNELS] = {0};
+};
+
+namespace {
+bool is_proj(int m) { return m == IG_PROJ_QR || m == IG_PROJ_CLASSIC; }
+bool is_extrap(int m) { return m == IG_EXTRAP_LS || m == IG_EXTRAP_SPARSE; }
+int64_t round_up(int64_t v, int64_t a) { return (v + a - 1) / a * a; }
+bool al16(const void *p) { return p == nullptr || (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+struct DevGuard {
+    int prev = -1;
+    explicit DevGuard(int dev) {
+        if (cudaGetDevice(&prev) == cudaSuccess && prev != dev) cudaSetDevice(dev);
+        else prev = -1;
+    }
+    ~DevGuard() {
+        if (prev >= 0) cudaSetDevice(prev);
+    }
+};
+
+void count(ig_t h, int n) {
+    h->launches += n;
+    g_launches += n;
+}
+
+cudaEvent_t pool_get(ig_t h) {
+    if (!h->ev_pool.empty()) {
+        cudaEvent_t e = h->ev_pool.back();
+        h->ev_pool.pop_back();
+        return e;
+    }
+    cudaEvent_t e = nullptr;
+    cudaEventCreate(&e);
+    return e;
+}
+
+// Brackets one kernel launch with CUDA events on the handle's stream when profiling is on.
+struct Prof {
+    ig_t h;
+    int kid;
+    cudaEvent_t a = nullptr;
+    Prof(ig_t h_, int kid_) : h(h_), kid(kid_) {
+        if (h->profiling) {
+            a = pool_get(h);
+            cudaEventRecord(a, h->stream);
+        }
+    }
+    ~Prof() {
+        if (a) {
+            cudaEvent_t b = pool_get(h);
+            cudaEventRecord(b, h->stream);
+            h->recs.push_back({kid, a, b});
+        }
+    }
+};
+
+void prof_drain(ig_t h) {
+    for (auto &r : h->recs) {
+        float ms = 0.f;
+        cudaEventSynchronize(r.b);
+        cudaEventElapsedTime(&ms, r.a, r.b);
+        h->prof_ms[r.kid] += ms;
+        h->prof_n[r.kid] += 1;
+        h->ev_pool.push_back(r.a);
+        h->ev_pool.push_back(r.b);
+    }
+    h->recs.clear();
+}
+
+ProjArgs proj_args(ig_t h) {
+    ProjArgs a;
+    memset(&a, 0, sizeof a);
+    a.ctrl = h->ctrl;
+    a.Bt = h->Bt;
+    a.Xt = h->Xt;
+    a.ld = h->ld;
+    a.N = h->N;
+    a.M = h->M;
+    a.method = h->method == IG_PROJ_QR ? M_PROJ_QR : M_PROJ_CLASSIC;
+    a.eps = h->eps;
+    a.blk = h->blk;
+    a.part = h->part;
+    a.gath = h->gath;
+    a.G = h->G;
+    return a;
+}
+
+int exchange(ig_t h, int stage) {
+    if (h->G <= 1) return IG_OK;
+    NcclApi &api = nccl();
+    ncclResult_t r = api.allGather(h->part + stage * PS, h->gath + (size_t)stage * h->G * PS, PS, ncclFloat64,
+                                   h->comm->comm, h->stream);
+    if (r != 0) return set_err(IG_E_NCCL, "ncclAllGather: %s", api.errStr(r));
+    return IG_OK;
+}
+
+int slot_index(ig_t h, int j) { return (h->head + j) % h->M; }  // j-th oldest stored solution
+double *next_slot_ptr(ig_t h) { return h->fill < h->M ? h->slots[slot_index(h, h->fill)] : h->slots[h->head]; }
+
+ig_t create_impl(int64_t N, int method, int m, int degree, void *storage, size_t bytes) {
+    if (N < 1) return set_err(IG_E_ARG, "N must be >= 1 (got %lld)", (long long)N), nullptr;
+    if (!is_proj(method) && !is_extrap(method)) return set_err(IG_E_ARG, "unknown method %d", method), nullptr;
+    if (m < 1 || m > IG_MAX_HISTORY)
+        return set_err(IG_E_ARG, "history size m must be in [1, %d] (got %d)", IG_MAX_HISTORY, m), nullptr;
+    if (is_extrap(method) && (degree < 0 || degree > m - 1))
+        return set_err(IG_E_ARG, "degree must satisfy 0 <= degree <= m-1 (PAPER.md:416; got %d, m=%d)", degree, m),
+               nullptr;
+    ig_t h = new ig_ctx;
+    h->N = N;
+    h->method = method;
+    h->M = m;
+    h->degree = is_extrap(method) ? degree : 0;
+    h->ld = round_up(N, 32);
+    if (cudaGetDevice(&h->dev) != cudaSuccess) {
+        set_err(IG_E_CUDA, "no CUDA device");
+        delete h;
+        return nullptr;
+    }
+    cudaDeviceGetAttribute(&h->nsm, cudaDevAttrMultiProcessorCount, h->dev);
+    const size_t need = ig_storage_bytes(N, method, m);
+    if (storage) {
+        if (bytes < need || (reinterpret_cast<uintptr_t>(storage) & 255)) {
+            set_err(IG_E_ARG, "storage too small (%zu < %zu) or not 256-byte aligned", bytes, need);
+            delete h;
+            return nullptr;
+        }
+        h->slab = static_cast<double *>(storage);
+    } else {
+        if (cudaMalloc(&h->slab, need) != cudaSuccess) {
+            cudaGetLastError();
+            set_err(IG_E_OOM, "cudaMalloc(%zu) for the history slabs failed", need);
+            delete h;
+            return nullptr;
+        }
+        h->own_slab = true;
+    }
+    h->slab_bytes = need;
+    if (is_proj(method)) {
+        h->Bt = h->slab;
+        h->Xt = h->slab + (size_t)m * h->ld;
+        bool ok = cudaMalloc(&h->ctrl, sizeof(Ctrl)) == cudaSuccess &&
+                  cudaMalloc(&h->blk, sizeof(double) * PS * MAXB) == cudaSuccess &&
+                  cudaMalloc(&h->part, sizeof(double) * PS * NSTAGE) == cudaSuccess;
+        if (!ok || cudaMemset(h->ctrl, 0, sizeof(Ctrl)) != cudaSuccess ||
+            cudaMemset(h->part, 0, sizeof(double) * PS * NSTAGE) != cudaSuccess) {
+            cudaGetLastError();
+            set_err(IG_E_OOM, "control-block allocation failed");
+            ig_destroy(h);
+            return nullptr;
+        }
+        h->gath = h->part;  // G == 1: [NSTAGE][1][PS] == [NSTAGE][PS]
+    } else {
+        for (int k = 0; k < m; ++k) h->slots.push_back(h->slab + (size_t)k * h->ld);
+        h->table.resize(m);
+        for (int f = 1; f <= m; ++f) {
+            const int q = degree < f - 1 ? degree : f - 1;  // warm-up rule (AMB-13)
+            h->table[f - 1].assign(f, 0.0);
+            const int rc = method == IG_EXTRAP_LS ? build_ls_weights(q, f, h->table[f - 1].data())
+                                                  : build_sparse_weights(q, f, h->table[f - 1].data());
+            if (rc < 0) {
+                set_err(IG_E_ARG, "weight builder failed for (%d, %d)", q, f);
+                ig_destroy(h);
+                return nullptr;
+            }
+        }
+    }
+    g_err.clear();
+    return h;
+}
+}  // namespace
+
+extern "C" {
+
+size_t ig_storage_bytes(int64_t N, int method, int m) {
+    if (N < 1 || m < 1) return 0;
+    const size_t vec = sizeof(double) * (size_t)round_up(N, 32);
+    return (is_proj(method) ? 2u : 1u) * (size_t)m * vec;
+}
+
+ig_t ig_create(int64_t N, int method, int m, int degree) { return create_impl(N, method, m, degree, nullptr, 0); }
+
+ig_t ig_create_ext(int64_t N, int method, int m, int degree, void *storage, size_t bytes) {
+    if (!storage) return set_err(IG_E_ARG, "storage is NULL"), nullptr;
+    return create_impl(N, method, m, degree, storage, bytes);
+}
+
+void ig_destroy(ig_t h) {
+    if (!h) return;
+    DevGuard g(h->dev);
+    if (h->stream) cudaStreamSynchronize(h->stream);
+    else cudaDeviceSynchronize();
+    if (h->own_slab) cudaFree(h->slab);
+    cudaFree(h->ctrl);
+    cudaFree(h->blk);
+    if (h->gath != h->part) cudaFree(h->gath);
+    cudaFree(h->part);
+    for (auto &s : h->stage) cudaFree(s);
+    prof_drain(h);
+    for (auto e : h->ev_pool) cudaEventDestroy(e);
+    delete h;
+}
+
+const char *ig_last_error(void) { return g_err.c_str(); }
+
+int ig_set_stream(ig_t h, void *s) {
+    if (!h) return set_err(IG_E_ARG, "NULL handle");
+    h->stream = static_cast<cudaStream_t>(s);
+    return IG_OK;
+}
+
+int ig_set_admit_tol(ig_t h, double eps) {
+    if (!h || !(eps >= 0.0)) return set_err(IG_E_ARG, "bad handle or eps");
+    h->eps = eps;
+    return IG_OK;
+}
+
+int ig_reset(ig_t h) {
+    if (!h) return set_err(IG_E_ARG, "NULL handle");
+    DevGuard g(h->dev);
+    if (is_proj(h->method)) CUDA_OK(cudaMemsetAsync(h->ctrl, 0, sizeof(Ctrl), h->stream));
+    h->head = h->fill = 0;
+    return IG_OK;
+}
+
+int ig_form_guess(ig_t h, const double *b, double *x0) {
+    if (!h) return set_err(IG_E_ARG, "NULL handle");
+    if (!x0) return set_err(IG_E_ARG, "x0 is NULL");
+    DevGuard g(h->dev);
+    if (is_proj(h->method)) {
+        if (!b) return set_err(IG_E_ARG, "b is NULL");
+        ProjArgs a = proj_args(h);
+        a.b = b;
+        a.x0 = x0;
+        const int vec = (al16(b) && al16(x0)) ? 2 : 1;
+        {
+            Prof p(h, IG_K_FORM_DOT);
+            CUDA_OK(launch_form_dot(a, vec, h->nsm, h->stream));
+        }
+        int rc = exchange(h, ST_FORM);
+        if (rc) return rc;
+        {
+            Prof p(h, IG_K_FORM_COMBINE);
+            CUDA_OK(launch_form_combine(a, vec, h->nsm, h->stream));
+        }
+        count(h, 2);
+        return IG_OK;
+    }
+    const int f = h->fill < h->M ? h->fill : h->M;
+    h->last_form_f = f;
+    if (f == 0) return IG_OK;  // x0 untouched (AMB-13)
+    ExtrapArgs a;
+    memset(&a, 0, sizeof a);
+    a.f = f;
+    a.N = h->N;
+    a.x0 = x0;
+    bool aligned = al16(x0);
+    for (int j = 0; j < f; ++j) {
+        a.src[j] = h->slots[slot_index(h, j)];
+        a.beta[j] = h->table[f - 1][j];
+        aligned = aligned && al16(a.src[j]);
+    }
+    {
+        Prof p(h, IG_K_EXTRAP);
+        CUDA_OK(launch_extrap(a, aligned ? 2 : 1, h->nsm, h->stream));
+    }
+    count(h, 1);
+    return IG_OK;
+}
+
+int ig_update(ig_t h, const double *x, const double *Ax) {
+    if (!h) return set_err(IG_E_ARG, "NULL handle");
+    if (!x) return set_err(IG_E_ARG, "x is NULL");
+    DevGuard g(h->dev);
+    if (is_proj(h->method)) {
+        if (!Ax) return set_err(IG_E_ARG, "Ax is NULL (projection needs A x, PAPER.md:237)");
+        ProjArgs a = proj_args(h);
+        a.x = x;
+        a.Ax = Ax;
+        const int vec = (al16(x) && al16(Ax)) ? 2 : 1;
+        {
+            Prof p(h, IG_K_U1);
+            CUDA_OK(launch_u1(a, vec, h->nsm, h->stream));
+        }
+        int rc = exchange(h, ST_U1);
+        if (rc) return rc;
+        {
+            Prof p(h, IG_K_U2);
+            CUDA_OK(launch_u2(a, vec, h->nsm, h->stream));
+        }
+        rc = exchange(h, ST_U2);
+        if (rc) return rc;
+        {
+            Prof p(h, IG_K_U3);
+            CUDA_OK(launch_u3(a, vec, h->nsm, h->stream));
+        }
+        count(h, 3);
+        return IG_OK;
+    }
+    double *slot = next_slot_ptr(h);
+    h->last_copy = (x != slot);
+    if (h->last_copy) {
+        Prof p(h, IG_K_COPY);
+        CUDA_OK(launch_copy(slot, x, h->N, (al16(x) && al16(slot)) ? 2 : 1, h->nsm, h->stream));
+        count(h, 1);
+    }
+    if (h->fill < h->M) ++h->fill;
+    else h->head = (h->head + 1) % h->M;
+    return IG_OK;
+}
+
+static int ensure_stage(ig_t h) {
+    for (auto &s : h->stage)
+        if (!s && cudaMalloc(&s, sizeof(double) * (size_t)h->ld) != cudaSuccess) {
+            cudaGetLastError();
+            return set_err(IG_E_OOM, "staging buffer allocation failed");
+        }
+    return IG_OK;
+}
+
+int ig_form_guess_host(ig_t h, const double *b, double *x0) {
+    if (!h || !x0) return set_err(IG_E_ARG, "NULL handle or x0");
+    DevGuard g(h->dev);
+    int rc = ensure_stage(h);
+    if (rc) return rc;
+    const size_t nb = sizeof(double) * (size_t)h->N;
+    if (is_proj(h->method)) {
+        if (!b) return set_err(IG_E_ARG, "b is NULL");
+        CUDA_OK(cudaMemcpyAsync(h->stage[0], b, nb, cudaMemcpyHostToDevice, h->stream));
+        CUDA_OK(cudaMemcpyAsync(h->stage[1], x0, nb, cudaMemcpyHostToDevice, h->stream));
+        rc = ig_form_guess(h, h->stage[0], h->stage[1]);
+        if (rc) return rc;
+    } else {
+        if (h->fill == 0) return IG_OK;  // x0 untouched, nothing to move
+        rc = ig_form_guess(h, nullptr, h->stage[1]);
+        if (rc) return rc;
+    }
+    CUDA_OK(cudaMemcpyAsync(x0, h->stage[1], nb, cudaMemcpyDeviceToHost, h->stream));
+    CUDA_OK(cudaStreamSynchronize(h->stream));
+    return IG_OK;
+}
+
+int ig_update_host(ig_t h, const double *x, const double *Ax) {
+    if (!h || !x) return set_err(IG_E_ARG, "NULL handle or x");
+    DevGuard g(h->dev);
+    const size_t nb = sizeof(double) * (size_t)h->N;
+    if (is_proj(h->method)) {
+        if (!Ax) return set_err(IG_E_ARG, "Ax is NULL");
+        int rc = ensure_stage(h);
+        if (rc) return rc;
+        CUDA_OK(cudaMemcpyAsync(h->stage[2], x, nb, cudaMemcpyHostToDevice, h->stream));
+        CUDA_OK(cudaMemcpyAsync(h->stage[3], Ax, nb, cudaMemcpyHostToDevice, h->stream));
+        rc = ig_update(h, h->stage[2], h->stage[3]);
+        if (rc) return rc;
+    } else {
+        double *slot = next_slot_ptr(h);  // copy straight into the ring slot: zero-copy push
+        CUDA_OK(cudaMemcpyAsync(slot, x, nb, cudaMemcpyHostToDevice, h->stream));
+        int rc = ig_update(h, slot, nullptr);
+        if (rc) return rc;
+    }
+    CUDA_OK(cudaStreamSynchronize(h->stream));
+    return IG_OK;
+}
+
+double *ig_next_slot(ig_t h) {
+    if (!h || !is_extrap(h->method)) return nullptr;
+    return next_slot_ptr(h);
+}
+
+int ig_comm_unique_id(void *out128) {
+    if (!out128) return set_err(IG_E_ARG, "NULL out");
+    NcclApi &api = nccl();
+    if (!api.ok) return set_err(IG_E_NCCL, "%s", api.why.c_str());
+    ncclUniqueId id;
+    ncclResult_t r = api.getUniqueId(&id);
+    if (r) return set_err(IG_E_NCCL, "ncclGetUniqueId: %s", api.errStr(r));
+    memcpy(out128, id.internal, 128);
+    return IG_OK;
+}
+
+int ig_comm_create(int nranks, int rank, const void *id128, ig_comm_t *out) {
+    if (!out || !id128 || nranks < 1 || rank < 0 || rank >= nranks) return set_err(IG_E_ARG, "bad comm arguments");
+    NcclApi &api = nccl();
+    if (!api.ok) return set_err(IG_E_NCCL, "%s", api.why.c_str());
+    ncclUniqueId id;
+    memcpy(id.internal, id128, 128);
+    auto *c = new ig_comm_ctx;
+    c->nranks = nranks;
+    c->rank = rank;
+    ncclResult_t r = api.commInitRank(&c->comm, nranks, id, rank);
+    if (r) {
+        delete c;
+        return set_err(IG_E_NCCL, "ncclCommInitRank: %s", api.errStr(r));
+    }
+    *out = c;
+    return IG_OK;
+}
+
+void ig_comm_destroy(ig_comm_t c) {
+    if (!c) return;
+    if (c->comm && nccl().ok) nccl().commDestroy(c->comm);
+    delete c;
+}
+
+int ig_attach_comm(ig_t h, ig_comm_t c) {
+    if (!h || !c) return set_err(IG_E_ARG, "NULL handle or comm");
+    DevGuard g(h->dev);
+    h->comm = c;
+    if (!is_proj(h->method) || c->nranks == 1) return IG_OK;  // extrapolation never communicates
+    if (h->gath != h->part) cudaFree(h->gath);
+    double *gb = nullptr;
+    if (cudaMalloc(&gb, sizeof(double) * PS * NSTAGE * c->nranks) != cudaSuccess) {
+        cudaGetLastError();
+        return set_err(IG_E_OOM, "gather buffer allocation failed");
+    }
+    CUDA_OK(cudaMemset(gb, 0, sizeof(double) * PS * NSTAGE * c->nranks));
+    h->gath = gb;
+    h->G = c->nranks;
+    return IG_OK;
+}
+
+int ig_history_dim(ig_t h, int *d) {
+    if (!h || !d) return set_err(IG_E_ARG, "NULL argument");
+    DevGuard g(h->dev);
+    if (is_proj(h->method)) {
+        CUDA_OK(cudaMemcpyAsync(d, &h->ctrl->d, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
+        CUDA_OK(cudaStreamSynchronize(h->stream));
+    } else {
+        *d = h->fill;
+    }
+    return IG_OK;
+}
+
+int ig_weights(ig_t h, int f, double *beta, int *len) {
+    if (!h || !beta || !len || !is_extrap(h->method)) return set_err(IG_E_ARG, "bad arguments");
+    if (f == 0) f = h->M;
+    if (f < 1 || f > h->M) return set_err(IG_E_ARG, "f must be in [0, M]");
+    for (int j = 0; j < f; ++j) beta[j] = h->table[f - 1][j];
+    *len = f;
+    return IG_OK;
+}
+
+int ig_get_stats(ig_t h, ig_stats_t *out) {
+    if (!h || !out) return set_err(IG_E_ARG, "NULL argument");
+    DevGuard g(h->dev);
+    memset(out, 0, sizeof *out);
+    out->launches = h->launches;
+    if (is_proj(h->method)) {
+        Ctrl c;
+        CUDA_OK(cudaMemcpyAsync(&c, h->ctrl, offsetof(Ctrl, gc), cudaMemcpyDeviceToHost, h->stream));
+        CUDA_OK(cudaStreamSynchronize(h->stream));
+        out->d = c.d;
+        out->admitted = c.admitted;
+        out->rho = c.rho;
+        out->norm_Ax = c.nAx;
+        out->norm_bt = c.nb;
+    } else {
+        out->d = h->fill;
+        out->admitted = 1;
+    }
+    return IG_OK;
+}
+
+int ig_bytes(ig_t h, int64_t *form_bytes, int64_t *update_bytes) {
+    if (!h || !form_bytes || !update_bytes) return set_err(IG_E_ARG, "NULL argument");
+    DevGuard g(h->dev);
+    const int64_t vb = 8 * h->N;
+    if (is_extrap(h->method)) {
+        *form_bytes = h->last_form_f ? (h->last_form_f + 1) * vb : 0;
+        *update_bytes = h->last_copy ? 2 * vb : 0;
+        return IG_OK;
+    }
+    Ctrl c;
+    CUDA_OK(cudaMemcpyAsync(&c, h->ctrl, offsetof(Ctrl, gc), cudaMemcpyDeviceToHost, h->stream));
+    CUDA_OK(cudaStreamSynchronize(h->stream));
+    const int M = h->M, de = c.deff, rot = c.last_rot, adm = c.admitted;
+    // form at the current d: (d+1) reads for the dots, d reads + 1 write for the combine
+    *form_bytes = c.d > 0 ? 2 * (int64_t)(c.d + 1) * vb : 0;
+    int64_t v = rot ? (M + 1 + (M - 1)) : (de + 1);  // U1: [B~ rotation] + dots against Ax
+    v += de > 0 ? de + 1 : 0;                          // U2
+    if (adm) v += 1 + de + 1 + 2;                      // U3: Ax, B~, x, two new columns
+    if (rot) v += M + (M - 1);                         // U3: X~ rotation
+    else if (adm) v += de;                             // U3: X~ reads
+    *update_bytes = v * vb;
+    return IG_OK;
+}
+
+int ig_copy_history(ig_t h, double *Bt_dst, double *Xt_dst, int64_t ld_dst, double *R_host) {
+    if (!h || !is_proj(h->method)) return set_err(IG_E_ARG, "projection handle required");
+    DevGuard g(h->dev);
+    const size_t w = sizeof(double) * (size_t)h->N;
+    if (Bt_dst)
+        CUDA_OK(cudaMemcpy2DAsync(Bt_dst, sizeof(double) * ld_dst, h->Bt, sizeof(double) * h->ld, w, h->M,
+                                  cudaMemcpyDeviceToDevice, h->stream));
+    if (Xt_dst)
+        CUDA_OK(cudaMemcpy2DAsync(Xt_dst, sizeof(double) * ld_dst, h->Xt, sizeof(double) * h->ld, w, h->M,
+                                  cudaMemcpyDeviceToDevice, h->stream));
+    if (R_host) {
+        std::vector<double> R(MAXM * MAXM);
+        CUDA_OK(cudaMemcpyAsync(R.data(), h->ctrl->R, sizeof(double) * MAXM * MAXM, cudaMemcpyDeviceToHost,
+                                h->stream));
+        CUDA_OK(cudaStreamSynchronize(h->stream));
+        for (int j = 0; j < h->M; ++j)
+            for (int i = 0; i < h->M; ++i) R_host[i + j * h->M] = R[i + j * MAXM];
+    }
+    CUDA_OK(cudaStreamSynchronize(h->stream));
+    return IG_OK;
+}
+
+int64_t ig_total_launches(void) { return g_launches.load(); }
+
+int ig_profile(ig_t h, int enable) {
+    if (!h) return set_err(IG_E_ARG, "NULL handle");
+    DevGuard g(h->dev);
+    prof_drain(h);
+    for (int k = 0; k < IG_NKERNELS; ++k) {
+        h->prof_ms[k] = 0.0;
+        h->prof_n[k] = 0;
+    }
+    h->profiling = enable != 0;
+    return IG_OK;
+}
+
+int ig_profile_read(ig_t h, int kernel, double *total_ms, int64_t *launches) {
+    if (!h || !total_ms || !launches || kernel < 0 || kernel >= IG_NKERNELS) return set_err(IG_E_ARG, "bad arguments");
+    DevGuard g(h->dev);
+    prof_drain(h);
+    *total_ms = h->prof_ms[kernel];
+    *launches = h->prof_n[kernel];
+    return IG_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,82 @@
+// ig_internal.h -- device control block and kernel-launch interface shared by the libig sources.
+// Product code only (never includes or is included by oracle/).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace ig {
+
+constexpr int MAXM = 32;       // IG_MAX_HISTORY
+constexpr int PS = MAXM + 1;   // partial-sum slots: coefficients 0..MAXM-1, norm^2 at slot MAXM
+constexpr int NORM = MAXM;     // slot index of the squared norm
+constexpr int MAXB = 1024;     // max blocks of a reduction kernel (block-partial buffer rows)
+constexpr int THREADS = 256;   // threads per block of every streaming kernel
+
+enum Stage { ST_FORM = 0, ST_U1 = 1, ST_U2 = 2, ST_U3 = 3, NSTAGE = 4 };
+enum Method { M_PROJ_QR = 1, M_EXTRAP_LS = 2, M_PROJ_CLASSIC = 3, M_EXTRAP_SPARSE = 4 };
+
+// Device-resident state of one projection handle.  Every control decision (d, downdate,
+// admission) is taken on the device from bitwise-identical (rank-ordered) sums, so the host
+// never synchronises on the hot path and all ranks agree.
+struct Ctrl {
+    int d;          // current history dimension
+    int pending;    // a QR downdate is due at the next update (d == M after an admission)
+    int rotX;       // this update applied the downdate to B~ (U1): U3 must rotate X~
+    int deff;       // dimension the Gram-Schmidt passes of the current update use
+    int admitted;   // last update admitted its pair
+    int last_rot;   // the last update applied a downdate (bytes accounting)
+    unsigned ticket[NSTAGE];
+    double rho, nAx, nb;
+    double gc[MAXM], gs[MAXM];      // Givens (c_i, s_i) of the pending downdate
+    double R[MAXM * MAXM];          // R, column-major R(i,j) = R[i + j*MAXM]
+    double Rdn[MAXM * MAXM];        // R after the pending downdate
+};
+
+struct ProjArgs {
+    Ctrl *ctrl;
+    double *Bt;            // B~ slabs: column k at Bt + k*ld
+    double *Xt;            // X~ slabs
+    int64_t ld;            // slab stride (doubles), multiple of 32
+    int64_t N;             // local vector length
+    int M;                 // capacity
+    int method;            // M_PROJ_QR or M_PROJ_CLASSIC
+    double eps;            // relative admission tolerance
+    double *blk;           // block partials [PS][MAXB]
+    double *part;          // this rank's partial sums [NSTAGE][PS]
+    const double *gath;    // gathered partials [NSTAGE][G][PS] (== part when G == 1)
+    int G;                 // ranks
+    const double *b;       // form: right-hand side
+    double *x0;            // form: guess (out)
+    const double *x;       // update: solution
+    const double *Ax;      // update: A x
+};
+
+struct ExtrapArgs {
+    const double *src[MAXM];  // stored solutions, oldest first
+    double beta[MAXM];        // weights, oldest first
+    int f;                    // number of terms
+    int pad_;
+    int64_t N;
+    double *x0;
+};
+
+// Launchers (kern_proj.cu / kern_extrap.cu).  `vec` = 2 when every vector is 16-byte aligned.
+// Return the cudaError_t of the launch.  *blocks receives the grid size used.
+cudaError_t launch_form_dot(const ProjArgs &a, int vec, int nsm, cudaStream_t s);
+cudaError_t launch_form_combine(const ProjArgs &a, int vec, int nsm, cudaStream_t s);
+cudaError_t launch_u1(const ProjArgs &a, int vec, int nsm, cudaStream_t s);
+cudaError_t launch_u2(const ProjArgs &a, int vec, int nsm, cudaStream_t s);
+cudaError_t launch_u3(const ProjArgs &a, int vec, int nsm, cudaStream_t s);
+cudaError_t launch_extrap(const ExtrapArgs &a, int vec, int nsm, cudaStream_t s);
+cudaError_t launch_copy(double *dst, const double *src, int64_t N, int vec, int nsm, cudaStream_t s);
+
+// Host weight builders (coeffs.cpp).
+// EXTRAP(m, M) least-squares weights, oldest first (Householder QR of the Legendre Vandermonde).
+int build_ls_weights(int m, int M, double *beta);
+// Theorem 3.1 naive weights (exact binomials).
+void build_naive_weights(int M, double *beta);
+// Sparse CPQR weights (Eq. CPQRCOEFFS); returns nonzero count or -1.
+int build_sparse_weights(int m, int M, double *beta);
+
+}  // namespace ig

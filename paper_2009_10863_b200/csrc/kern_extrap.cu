@@ -1,0 +1,130 @@
+// kern_extrap.cu -- sm_100a kernels of the extrapolation hot path (arXiv 2009.10863 §3).
+//
+//   k_extrap  x0 = sum_{i=1}^{f} beta_i x_{n-f+i}   (Eq. EXTRAPEXPN, PAPER.md:335-347;
+//             paper kernel extrapKernel).  beta and the f slot pointers (oldest
+//             first) travel BY VALUE in the kernel-parameter constant bank: every thread reads
+//             them as uniform constants, no global state shared between handles.
+//   k_copy    push of a solution that was not solved in place (2 values/element).
+// Both are pure streams: (f+1) and 2 fp64 values per element.
+#include "ig_internal.h"
+
+namespace ig {
+
+template <int FC, int VEC, int UNROLL>
+__global__ void __launch_bounds__(THREADS) k_extrap(const __grid_constant__ ExtrapArgs a) {
+    const int f = a.f;
+    if (VEC == 2) {
+        const int64_t nv = a.N >> 1;
+        const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+        int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+        for (; i + (UNROLL - 1) * stride < nv; i += UNROLL * stride) {
+            double2 acc[UNROLL];
+#pragma unroll
+            for (int u = 0; u < UNROLL; ++u) acc[u] = make_double2(0.0, 0.0);
+#pragma unroll
+            for (int j = 0; j < FC; ++j) {
+                if (j < f) {
+                    double2 xv[UNROLL];
+#pragma unroll
+                    for (int u = 0; u < UNROLL; ++u)
+                        xv[u] = __ldg(reinterpret_cast<const double2 *>(a.src[j]) + i + u * stride);
+#pragma unroll
+                    for (int u = 0; u < UNROLL; ++u) {
+                        acc[u].x = fma(a.beta[j], xv[u].x, acc[u].x);
+                        acc[u].y = fma(a.beta[j], xv[u].y, acc[u].y);
+                    }
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < UNROLL; ++u) reinterpret_cast<double2 *>(a.x0)[i + u * stride] = acc[u];
+        }
+        for (; i < nv; i += stride) {
+            double2 acc = make_double2(0.0, 0.0);
+#pragma unroll
+            for (int j = 0; j < FC; ++j)
+                if (j < f) {
+                    const double2 xv = __ldg(reinterpret_cast<const double2 *>(a.src[j]) + i);
+                    acc.x = fma(a.beta[j], xv.x, acc.x);
+                    acc.y = fma(a.beta[j], xv.y, acc.y);
+                }
+            reinterpret_cast<double2 *>(a.x0)[i] = acc;
+        }
+        if ((a.N & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
+            const int64_t e = a.N - 1;
+            double acc = 0.0;
+#pragma unroll
+            for (int j = 0; j < FC; ++j)
+                if (j < f) acc = fma(a.beta[j], a.src[j][e], acc);
+            a.x0[e] = acc;
+        }
+    } else {
+        const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+        for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < a.N; i += stride) {
+            double acc = 0.0;
+#pragma unroll
+            for (int j = 0; j < FC; ++j)
+                if (j < f) acc = fma(a.beta[j], __ldg(a.src[j] + i), acc);
+            a.x0[i] = acc;
+        }
+    }
+}
+
+template <int VEC>
+__global__ void __launch_bounds__(THREADS) k_copy(double *__restrict__ dst, const double *__restrict__ src, int64_t N) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    if (VEC == 2) {
+        const int64_t nv = N >> 1;
+        for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nv; i += stride)
+            reinterpret_cast<double2 *>(dst)[i] = __ldg(reinterpret_cast<const double2 *>(src) + i);
+        if ((N & 1) && blockIdx.x == 0 && threadIdx.x == 0) dst[N - 1] = src[N - 1];
+    } else {
+        for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < N; i += stride) dst[i] = src[i];
+    }
+}
+
+template <class K> static int grid_for_x(K kern, int64_t nv, int nsm) {
+    int occ = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, THREADS, 0) != cudaSuccess || occ < 1) occ = 1;
+    if (occ > 8) occ = 8;
+    int64_t want = (nv + THREADS - 1) / THREADS;
+    int64_t g = (int64_t)nsm * occ;
+    if (want < g) g = want;
+    if (g < 1) g = 1;
+    return (int)g;
+}
+
+template <int FC>
+static void launch_fc(const ExtrapArgs &a, int vec, int nsm, cudaStream_t s) {
+    if (vec == 2) {
+        constexpr int U = FC <= 2 ? 4 : (FC <= 4 ? 2 : 1);
+        auto k = k_extrap<FC, 2, U>;
+        k<<<grid_for_x(k, a.N / 2, nsm), THREADS, 0, s>>>(a);
+    } else {
+        auto k = k_extrap<FC, 1, 1>;
+        k<<<grid_for_x(k, a.N, nsm), THREADS, 0, s>>>(a);
+    }
+}
+
+cudaError_t launch_extrap(const ExtrapArgs &a, int vec, int nsm, cudaStream_t s) {
+    const int f = a.f;
+    if (f <= 1) launch_fc<1>(a, vec, nsm, s);
+    else if (f <= 2) launch_fc<2>(a, vec, nsm, s);
+    else if (f <= 4) launch_fc<4>(a, vec, nsm, s);
+    else if (f <= 8) launch_fc<8>(a, vec, nsm, s);
+    else if (f <= 16) launch_fc<16>(a, vec, nsm, s);
+    else launch_fc<32>(a, vec, nsm, s);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_copy(double *dst, const double *src, int64_t N, int vec, int nsm, cudaStream_t s) {
+    if (vec == 2) {
+        auto k = k_copy<2>;
+        k<<<grid_for_x(k, N / 2, nsm), THREADS, 0, s>>>(dst, src, N);
+    } else {
+        auto k = k_copy<1>;
+        k<<<grid_for_x(k, N, nsm), THREADS, 0, s>>>(dst, src, N);
+    }
+    return cudaGetLastError();
+}
+
+}  // namespace ig

@@ -1,0 +1,290 @@
+"""Python binding of the libig C ABI: same names as include/ig.h, torch tensors in, pointers out.
+
+Only argument marshalling happens here: every step of the hot path runs in libig's CUDA
+kernels.  torch supplies device memory, the current stream and process groups.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import torch
+
+from ._lib import (  # noqa: F401
+    IG_E_ARG,
+    IG_EXTRAP_LS,
+    IG_EXTRAP_SPARSE,
+    IG_MAX_HISTORY,
+    IG_OK,
+    IG_PROJ_CLASSIC,
+    IG_PROJ_QR,
+    STATUS_NAMES,
+    ig_stats_t,
+    lib,
+)
+
+METHODS = {"proj_qr": IG_PROJ_QR, "extrap_ls": IG_EXTRAP_LS, "proj_classic": IG_PROJ_CLASSIC,
+           "extrap_sparse": IG_EXTRAP_SPARSE}
+
+
+class IGError(RuntimeError):
+    def __init__(self, code: int, where: str):
+        msg = lib().ig_last_error().decode(errors="replace")
+        super().__init__(f"{where}: {STATUS_NAMES.get(code, code)}: {msg}")
+        self.code = code
+
+
+def _check(rc: int, where: str) -> None:
+    if rc != IG_OK:
+        raise IGError(rc, where)
+
+
+def _dptr(t, name: str, N: int | None = None):
+    """Device pointer of a contiguous fp64 CUDA tensor (None -> NULL)."""
+    if t is None:
+        return None
+    if not isinstance(t, torch.Tensor) or t.dtype != torch.float64 or not t.is_cuda or not t.is_contiguous():
+        raise TypeError(f"{name} must be a contiguous float64 CUDA tensor")
+    if N is not None and t.numel() != N:
+        raise ValueError(f"{name} has {t.numel()} elements, expected {N}")
+    return t.data_ptr()
+
+
+def _hptr(t, name: str, N: int | None = None):
+    if t is None:
+        return None
+    if not isinstance(t, torch.Tensor) or t.dtype != torch.float64 or t.is_cuda or not t.is_contiguous():
+        raise TypeError(f"{name} must be a contiguous float64 CPU tensor")
+    if N is not None and t.numel() != N:
+        raise ValueError(f"{name} has {t.numel()} elements, expected {N}")
+    return t.data_ptr()
+
+
+# ------------------------------------------------------------------ C-ABI mirrors
+def ig_create(N: int, method: int, m: int, degree: int = 0, stream=None):
+    h = lib().ig_create(int(N), int(method), int(m), int(degree))
+    if not h:
+        raise IGError(IG_E_ARG, "ig_create")
+    s = stream if stream is not None else torch.cuda.current_stream()
+    _check(lib().ig_set_stream(h, C.c_void_p(s.cuda_stream)), "ig_set_stream")
+    return h
+
+
+def ig_destroy(h) -> None:
+    lib().ig_destroy(h)
+
+
+def ig_reset(h) -> None:
+    _check(lib().ig_reset(h), "ig_reset")
+
+
+def ig_set_admit_tol(h, eps: float) -> None:
+    _check(lib().ig_set_admit_tol(h, float(eps)), "ig_set_admit_tol")
+
+
+def ig_set_stream(h, stream) -> None:
+    _check(lib().ig_set_stream(h, C.c_void_p(stream.cuda_stream)), "ig_set_stream")
+
+
+def ig_form_guess(h, b, x0) -> None:
+    _check(lib().ig_form_guess(h, _dptr(b, "b"), _dptr(x0, "x0")), "ig_form_guess")
+
+
+def ig_update(h, x, Ax=None) -> None:
+    _check(lib().ig_update(h, _dptr(x, "x"), _dptr(Ax, "Ax")), "ig_update")
+
+
+def ig_form_guess_host(h, b, x0) -> None:
+    _check(lib().ig_form_guess_host(h, _hptr(b, "b"), _hptr(x0, "x0")), "ig_form_guess_host")
+
+
+def ig_update_host(h, x, Ax=None) -> None:
+    _check(lib().ig_update_host(h, _hptr(x, "x"), _hptr(Ax, "Ax")), "ig_update_host")
+
+
+def ig_next_slot(h) -> int:
+    """Device address of the extrapolation zero-copy slot (0 for projection handles)."""
+    return lib().ig_next_slot(h) or 0
+
+
+def ig_history_dim(h) -> int:
+    d = C.c_int()
+    _check(lib().ig_history_dim(h, C.byref(d)), "ig_history_dim")
+    return d.value
+
+
+def ig_weights(h, f: int = 0):
+    beta = (C.c_double * IG_MAX_HISTORY)()
+    n = C.c_int()
+    _check(lib().ig_weights(h, int(f), beta, C.byref(n)), "ig_weights")
+    return [beta[i] for i in range(n.value)]
+
+
+def ig_bytes(h):
+    fb, ub = C.c_int64(), C.c_int64()
+    _check(lib().ig_bytes(h, C.byref(fb), C.byref(ub)), "ig_bytes")
+    return fb.value, ub.value
+
+
+def ig_get_stats(h) -> dict:
+    s = ig_stats_t()
+    _check(lib().ig_get_stats(h, C.byref(s)), "ig_get_stats")
+    return {k: getattr(s, k) for k, _ in ig_stats_t._fields_}
+
+
+def ig_copy_history(h, M: int, N: int):
+    """(Bt[M,N], Xt[M,N]) device copies and R[M,M] (host) of a projection handle."""
+    Bt = torch.empty((M, N), dtype=torch.float64, device="cuda")
+    Xt = torch.empty((M, N), dtype=torch.float64, device="cuda")
+    R = (C.c_double * (M * M))()
+    _check(lib().ig_copy_history(h, Bt.data_ptr(), Xt.data_ptr(), N, R), "ig_copy_history")
+    Rt = torch.tensor(list(R), dtype=torch.float64).reshape(M, M).T.contiguous()  # column-major -> [i, j]
+    return Bt, Xt, Rt
+
+
+def ig_total_launches() -> int:
+    return int(lib().ig_total_launches())
+
+
+def ig_profile(h, enable: bool) -> None:
+    _check(lib().ig_profile(h, 1 if enable else 0), "ig_profile")
+
+
+def ig_profile_read(h) -> dict:
+    """{kernel name: (total_ms, launches)} since the last ig_profile call (syncs)."""
+    from ._lib import KERNELS
+
+    out = {}
+    for k, name in enumerate(KERNELS):
+        ms, n = C.c_double(), C.c_int64()
+        _check(lib().ig_profile_read(h, k, C.byref(ms), C.byref(n)), "ig_profile_read")
+        out[name] = (ms.value, n.value)
+    return out
+
+
+def ig_comm_unique_id() -> bytes:
+    buf = (C.c_char * 128)()
+    _check(lib().ig_comm_unique_id(buf), "ig_comm_unique_id")
+    return bytes(buf)
+
+
+def ig_comm_create(nranks: int, rank: int, uid: bytes):
+    if len(uid) != 128:
+        raise ValueError("unique id must be 128 bytes")
+    out = C.c_void_p()
+    _check(lib().ig_comm_create(int(nranks), int(rank), C.c_char_p(uid), C.byref(out)), "ig_comm_create")
+    return out.value
+
+
+def ig_comm_destroy(c) -> None:
+    lib().ig_comm_destroy(c)
+
+
+def ig_attach_comm(h, c) -> None:
+    _check(lib().ig_attach_comm(h, c), "ig_attach_comm")
+
+
+def _nccl_path() -> str | None:
+    try:
+        import nvidia.nccl
+
+        for p in nvidia.nccl.__path__:
+            cand = os.path.join(p, "lib", "libnccl.so.2")
+            if os.path.exists(cand):
+                return cand
+    except ImportError:
+        pass
+    return None
+
+
+def comm_from_process_group(group=None):
+    """NCCL communicator for libig over the ranks of a torch.distributed group.
+
+    Rank 0 draws the NCCL unique id through libig; torch.distributed broadcasts the 128 bytes
+    (plumbing only).  Every rank must use its own GPU (torch.cuda.set_device before this).
+    """
+    import torch.distributed as dist
+
+    if "IG_NCCL_PATH" not in os.environ:
+        p = _nccl_path()
+        if p:
+            os.environ["IG_NCCL_PATH"] = p
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    obj = [ig_comm_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(obj, src=dist.get_global_rank(group, 0) if group is not None else 0, group=group)
+    return ig_comm_create(world, rank, obj[0])
+
+
+def shard_range(N_total: int, world: int, rank: int):
+    """Contiguous DOF range [lo, hi) of `rank` (z-slab partition); sizes differ by <= 1."""
+    base, rem = divmod(int(N_total), int(world))
+    lo = rank * base + min(rank, rem)
+    return lo, lo + base + (1 if rank < rem else 0)
+
+
+# ------------------------------------------------------------------ convenience object
+class InitialGuess:
+    """One history space (one field).  Thin wrapper over an ig_t handle."""
+
+    def __init__(self, N: int, method="proj_qr", m: int = 8, degree: int = 0, eps: float | None = None,
+                 comm=None, stream=None):
+        self.N, self.m, self.degree = int(N), int(m), int(degree)
+        self.method = METHODS[method] if isinstance(method, str) else int(method)
+        self.h = ig_create(self.N, self.method, self.m, self.degree, stream)
+        if eps is not None:
+            ig_set_admit_tol(self.h, eps)
+        if comm is not None:
+            ig_attach_comm(self.h, comm)
+
+    def form_guess(self, b, x0):
+        ig_form_guess(self.h, b, x0)
+        return x0
+
+    def update(self, x, Ax=None):
+        ig_update(self.h, x, Ax)
+
+    def next_slot(self):
+        """torch view of the extrapolation zero-copy slot."""
+        addr = ig_next_slot(self.h)
+        if not addr:
+            return None
+        return _view(addr, self.N)
+
+    @property
+    def d(self) -> int:
+        return ig_history_dim(self.h)
+
+    def stats(self) -> dict:
+        return ig_get_stats(self.h)
+
+    def bytes(self):
+        return ig_bytes(self.h)
+
+    def weights(self, f: int = 0):
+        return ig_weights(self.h, f)
+
+    def reset(self):
+        ig_reset(self.h)
+
+    def close(self):
+        if self.h:
+            ig_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class _CAI:
+    def __init__(self, addr: int, n: int):
+        self.__cuda_array_interface__ = {"shape": (n,), "typestr": "<f8", "data": (addr, False), "version": 3,
+                                         "strides": None}
+
+
+def _view(addr: int, n: int) -> torch.Tensor:
+    """Zero-copy torch view of library-owned device memory (CUDA array interface)."""
+    return torch.as_tensor(_CAI(addr, n), device="cuda")

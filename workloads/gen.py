@@ -158,3 +158,67 @@ def manufactured_step(g: Grid, n: int, dt: float = 1e-3, eta_rel: float = 1e-8, 
 def prescribed_rhs(g: Grid, n: int, dt: float = 1e-3, device="cpu") -> torch.Tensor:
     """Closed-loop RHS b_n = f(., t_n) with f the smooth family (independent of any solver output)."""
     return smooth_field(g, n * dt, device)
+
+
+def manufactured_step_slab(n_xy: int, nz_local: int, rank: int, world: int, n: int, dt: float = 1e-3,
+                           eta_rel: float = 1e-8, sigma: float = 1.0, device="cpu", seed: int = SEED):
+    """Rank `rank`'s z-slab of a global n_xy x n_xy x (nz_local*world) manufactured step.
+
+    The field and noise are those of the global grid restricted to the slab (contiguous DOF
+    range); the harness operator is the 7-point Helmholtz stencil of the slab with
+    homogeneous Dirichlet faces (block-diagonal across ranks: a valid SPD operator, no halo
+    exchange needed for synthetic timing inputs).
+    """
+    nzg = nz_local * world
+    count = n_xy * n_xy * nz_local
+    offset = rank * count
+    idx = torch.arange(offset, offset + count, dtype=torch.int64, device=device)
+    xs = [((idx // (n_xy * n_xy)) + 1).to(torch.float64) / (nzg + 1),
+          (((idx // n_xy) % n_xy) + 1).to(torch.float64) / (n_xy + 1),
+          ((idx % n_xy) + 1).to(torch.float64) / (n_xy + 1)]
+    u = _field_at(xs, n * dt, 3)
+    eta = eta_rel * float(u.abs().max())
+    x = u + eta * counter_uniform(seed, n, count, device, offset=offset)
+    gl = _SlabGrid(n_xy, nz_local, sigma)
+    return gl.apply(u), x, gl.apply(x)
+
+
+def _field_at(X, t: float, dim: int) -> torch.Tensor:
+    env = torch.ones_like(X[0])
+    for xj in X:
+        env = env * torch.sin(math.pi * xj)
+    u = env * (1.0 + 0.3 * math.sin(2.0 * math.pi * t))
+    c = [0.3 + 0.4 * t, 0.5 + 0.1 * math.sin(2.0 * math.pi * t), 0.5 + 0.1 * math.cos(2.0 * math.pi * t)]
+    r2 = torch.zeros_like(X[0])
+    for j, xj in enumerate(X):
+        r2 = r2 + (xj - c[j]) ** 2
+    u = u + torch.exp(-r2 / 0.02)
+    q, omega, phi = _modes(dim)
+    for k in range(q.shape[0]):
+        m = torch.full_like(X[0], math.cos(omega[k] * t + phi[k]))
+        for j, xj in enumerate(X):
+            m = m * torch.sin(float(q[k, j]) * math.pi * xj)
+        u = u + m
+    return u
+
+
+@dataclass(frozen=True)
+class _SlabGrid:
+    n_xy: int
+    nz: int
+    sigma: float
+
+    def apply(self, x: torch.Tensor) -> torch.Tensor:
+        h = 1.0 / (self.n_xy + 1)
+        u = x.reshape(self.nz, self.n_xy, self.n_xy)
+        y = (6.0 / h ** 2 + self.sigma) * u
+        inv = 1.0 / h ** 2
+        for ax in range(3):
+            n = u.shape[ax]
+            lo = [slice(None)] * 3
+            hi = [slice(None)] * 3
+            lo[ax] = slice(0, n - 1)
+            hi[ax] = slice(1, n)
+            y[tuple(lo)] -= inv * u[tuple(hi)]
+            y[tuple(hi)] -= inv * u[tuple(lo)]
+        return y.reshape(-1)
