@@ -330,7 +330,7 @@ def run_ours(args, world, rank, local):
                 "step_frac": (step_bytes / (ms_per_step * 1e-3) / 1e9) / peak}
 
     # ---- end to end through the public host-buffer API (H2D of inputs and D2H of guesses timed)
-    P = min(4, S)
+    P = min(4, K)
     host = [tuple(t.cpu().pin_memory() for t in pool[prefill + W + j]) for j in range(P)]
     x0h_p = torch.zeros(N, dtype=torch.float64).pin_memory()
     x0h_e = torch.zeros(N, dtype=torch.float64).pin_memory()

@@ -6,71 +6,60 @@
 //             them as uniform constants, no global state shared between handles.
 //   k_copy    push of a solution that was not solved in place (2 values/element).
 // Both are pure streams: (f+1) and 2 fp64 values per element.
+#include <type_traits>
+
 #include "ig_internal.h"
 
 namespace ig {
 
 template <int FC, int VEC, int UNROLL>
-__global__ void __launch_bounds__(THREADS) k_extrap(const __grid_constant__ ExtrapArgs a) {
+__global__ void __launch_bounds__(THREADS, 1) k_extrap(const __grid_constant__ ExtrapArgs a) {
+    // All loads of a trip are issued before the FMAs consume them (see kern_proj.cu); the
+    // accumulation order is oldest -> newest, like Eq. EXTRAPEXPN.
+    typedef typename std::conditional<VEC == 2, double2, double>::type V;
     const int f = a.f;
-    if (VEC == 2) {
-        const int64_t nv = a.N >> 1;
-        const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-        int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-        for (; i + (UNROLL - 1) * stride < nv; i += UNROLL * stride) {
-            double2 acc[UNROLL];
+    const int64_t nv = a.N / VEC;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i0 < nv; i0 += UNROLL * stride) {
+        V col[UNROLL][FC];
 #pragma unroll
-            for (int u = 0; u < UNROLL; ++u) acc[u] = make_double2(0.0, 0.0);
+        for (int u = 0; u < UNROLL; ++u) {
+            const int64_t i = i0 + u * stride;
+#pragma unroll
+            for (int j = 0; j < FC; ++j)
+                col[u][j] = (i < nv && j < f) ? __ldg(reinterpret_cast<const V *>(a.src[j]) + i) : V{};
+        }
+#pragma unroll
+        for (int u = 0; u < UNROLL; ++u) {
+            const int64_t i = i0 + u * stride;
+            V acc{};
 #pragma unroll
             for (int j = 0; j < FC; ++j) {
-                if (j < f) {
-                    double2 xv[UNROLL];
-#pragma unroll
-                    for (int u = 0; u < UNROLL; ++u)
-                        xv[u] = __ldg(reinterpret_cast<const double2 *>(a.src[j]) + i + u * stride);
-#pragma unroll
-                    for (int u = 0; u < UNROLL; ++u) {
-                        acc[u].x = fma(a.beta[j], xv[u].x, acc[u].x);
-                        acc[u].y = fma(a.beta[j], xv[u].y, acc[u].y);
-                    }
+                if (VEC == 2) {
+                    double *pa = reinterpret_cast<double *>(&acc);
+                    const double *pc = reinterpret_cast<const double *>(&col[u][j]);
+                    pa[0] = fma(a.beta[j], pc[0], pa[0]);
+                    pa[1] = fma(a.beta[j], pc[1], pa[1]);
+                } else {
+                    double *pa = reinterpret_cast<double *>(&acc);
+                    pa[0] = fma(a.beta[j], *reinterpret_cast<const double *>(&col[u][j]), pa[0]);
                 }
             }
-#pragma unroll
-            for (int u = 0; u < UNROLL; ++u) reinterpret_cast<double2 *>(a.x0)[i + u * stride] = acc[u];
+            if (i < nv) reinterpret_cast<V *>(a.x0)[i] = acc;
         }
-        for (; i < nv; i += stride) {
-            double2 acc = make_double2(0.0, 0.0);
+    }
+    if (VEC == 2 && (a.N & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
+        const int64_t e = a.N - 1;
+        double acc = 0.0;
 #pragma unroll
-            for (int j = 0; j < FC; ++j)
-                if (j < f) {
-                    const double2 xv = __ldg(reinterpret_cast<const double2 *>(a.src[j]) + i);
-                    acc.x = fma(a.beta[j], xv.x, acc.x);
-                    acc.y = fma(a.beta[j], xv.y, acc.y);
-                }
-            reinterpret_cast<double2 *>(a.x0)[i] = acc;
-        }
-        if ((a.N & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
-            const int64_t e = a.N - 1;
-            double acc = 0.0;
-#pragma unroll
-            for (int j = 0; j < FC; ++j)
-                if (j < f) acc = fma(a.beta[j], a.src[j][e], acc);
-            a.x0[e] = acc;
-        }
-    } else {
-        const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-        for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < a.N; i += stride) {
-            double acc = 0.0;
-#pragma unroll
-            for (int j = 0; j < FC; ++j)
-                if (j < f) acc = fma(a.beta[j], __ldg(a.src[j] + i), acc);
-            a.x0[i] = acc;
-        }
+        for (int j = 0; j < FC; ++j)
+            if (j < f) acc = fma(a.beta[j], a.src[j][e], acc);
+        a.x0[e] = acc;
     }
 }
 
 template <int VEC>
-__global__ void __launch_bounds__(THREADS) k_copy(double *__restrict__ dst, const double *__restrict__ src, int64_t N) {
+__global__ void __launch_bounds__(THREADS, 1) k_copy(double *__restrict__ dst, const double *__restrict__ src, int64_t N) {
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     if (VEC == 2) {
         const int64_t nv = N >> 1;
@@ -97,10 +86,11 @@ template <int FC>
 static void launch_fc(const ExtrapArgs &a, int vec, int nsm, cudaStream_t s) {
     if (vec == 2) {
         constexpr int U = FC <= 2 ? 4 : (FC <= 4 ? 2 : 1);
-        auto k = k_extrap<FC, 2, U>;
+        auto k = k_extrap<FC, 2, U>;  // U strided elements per trip when few streams
         k<<<grid_for_x(k, a.N / 2, nsm), THREADS, 0, s>>>(a);
     } else {
-        auto k = k_extrap<FC, 1, 1>;
+        constexpr int U = FC <= 2 ? 4 : (FC <= 4 ? 2 : 1);
+        auto k = k_extrap<FC, 1, U>;
         k<<<grid_for_x(k, a.N, nsm), THREADS, 0, s>>>(a);
     }
 }

@@ -96,17 +96,27 @@ __device__ __forceinline__ bool block_partials_ticket(const double (&v)[NV], int
     return last;
 }
 
-// Last block: out[k] = sum over blocks (fixed order per lane + fixed xor tree) of blk[k][*].
+// Last block: out[k] = sum over blocks of blk[k][*] in a fixed order: lane l owns blocks
+// l, l+32, ... accumulated 8-way (8 independent loads in flight), then a fixed xor tree.
 __device__ __forceinline__ void final_reduce(int nc, bool norm, const double *blk, double *out) {
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
     const int nb = gridDim.x;
     for (int k = w; k < PS; k += nw) {
         const bool act = (k < MAXM) ? (k < nc) : norm;
         if (!act) continue;
-        double s = 0.0;
-        for (int b = lane; b < nb; b += 32) s += __ldcg(&blk[k * MAXB + b]);
-        s = warp_sum(s);
-        if (lane == 0) out[k] = s;
+        const double *row = blk + k * MAXB;
+        double s[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) s[u] = 0.0;
+        int b = lane;
+        for (; b + 7 * 32 < nb; b += 8 * 32) {
+#pragma unroll
+            for (int u = 0; u < 8; ++u) s[u] += __ldcg(row + b + u * 32);
+        }
+        for (int u = 0; b < nb; b += 32, ++u) s[u] += __ldcg(row + b);
+        double t = ((s[0] + s[1]) + (s[2] + s[3])) + ((s[4] + s[5]) + (s[6] + s[7]));
+        t = warp_sum(t);
+        if (lane == 0) out[k] = t;
     }
 }
 
@@ -117,10 +127,20 @@ __device__ __forceinline__ double rank_sum(const double *g, int G, int k) {
     return s;
 }
 
+// All streaming loops follow one pattern: every load of a trip is issued before any
+// arithmetic consumes it (`col[]` arrays), and the kernels are compiled with
+// __launch_bounds__(THREADS, 1) so ptxas keeps them grouped instead of interleaving loads with
+// their DFMAs to save registers (which cut memory-level parallelism to ~2 loads per thread).
+// Streams with few vectors process U strided elements per trip for more bytes in flight.
+template <int MC> struct Unroll {
+    static constexpr int U = MC <= 2 ? 4 : (MC <= 4 ? 2 : 1);
+};
+
 // ------------------------------------------------------------------ form: alpha = B~^T b
 template <int MC, int VEC>
-__global__ void __launch_bounds__(THREADS) k_form_dot(ProjArgs a) {
+__global__ void __launch_bounds__(THREADS, 1) k_form_dot(ProjArgs a) {
     typedef typename VT<VEC>::T V;
+    constexpr int U = Unroll<MC>::U;
     __shared__ double sh[(THREADS / 32) * (MC + 1)];
     const int d = a.ctrl->d;
     if (d == 0) return;  // x0 is the caller's fallback
@@ -129,11 +149,20 @@ __global__ void __launch_bounds__(THREADS) k_form_dot(ProjArgs a) {
     for (int k = 0; k <= MC; ++k) v[k] = 0.0;
     const int64_t nv = a.N / VEC;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nv; i += stride) {
-        const V bv = ldro<V>(a.b, i);
+    for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i0 < nv; i0 += U * stride) {
+        V bv[U], col[U][MC];
 #pragma unroll
-        for (int k = 0; k < MC; ++k)
-            if (k < d) v[k] = vdot(ldro<V>(a.Bt + k * a.ld, i), bv, v[k]);
+        for (int u = 0; u < U; ++u) {
+            const int64_t i = i0 + u * stride;
+            const bool ok = i < nv;
+            bv[u] = ok ? ldro<V>(a.b, i) : vzero(V());
+#pragma unroll
+            for (int k = 0; k < MC; ++k) col[u][k] = (ok && k < d) ? ldro<V>(a.Bt + k * a.ld, i) : vzero(V());
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+#pragma unroll
+            for (int k = 0; k < MC; ++k) v[k] = vdot(col[u][k], bv[u], v[k]);
     }
     if (VEC == 2 && (a.N & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
         const int64_t i = a.N - 1;
@@ -150,8 +179,9 @@ __global__ void __launch_bounds__(THREADS) k_form_dot(ProjArgs a) {
 
 // ------------------------------------------------------------------ form: x0 = X~ alpha
 template <int MC, int VEC>
-__global__ void __launch_bounds__(THREADS) k_form_combine(ProjArgs a) {
+__global__ void __launch_bounds__(THREADS, 1) k_form_combine(ProjArgs a) {
     typedef typename VT<VEC>::T V;
+    constexpr int U = Unroll<MC>::U;
     __shared__ double s_al[MC];
     const int d = a.ctrl->d;
     if (d == 0) return;
@@ -163,12 +193,22 @@ __global__ void __launch_bounds__(THREADS) k_form_combine(ProjArgs a) {
     for (int k = 0; k < MC; ++k) al[k] = (k < d) ? s_al[k] : 0.0;
     const int64_t nv = a.N / VEC;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nv; i += stride) {
-        V acc = vzero(V());
+    for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i0 < nv; i0 += U * stride) {
+        V col[U][MC];
 #pragma unroll
-        for (int k = 0; k < MC; ++k)
-            if (k < d) acc = vaxpy(al[k], ldro<V>(a.Xt + k * a.ld, i), acc);
-        stv<V>(a.x0, i, acc);
+        for (int u = 0; u < U; ++u) {
+            const int64_t i = i0 + u * stride;
+#pragma unroll
+            for (int k = 0; k < MC; ++k) col[u][k] = (i < nv && k < d) ? ldro<V>(a.Xt + k * a.ld, i) : vzero(V());
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int64_t i = i0 + u * stride;
+            V acc = vzero(V());
+#pragma unroll
+            for (int k = 0; k < MC; ++k) acc = vaxpy(al[k], col[u][k], acc);
+            if (i < nv) stv<V>(a.x0, i, acc);
+        }
     }
     if (VEC == 2 && (a.N & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
         const int64_t i = a.N - 1;
@@ -184,15 +224,15 @@ __global__ void __launch_bounds__(THREADS) k_form_combine(ProjArgs a) {
 template <int MC, class V>
 __device__ __forceinline__ void u1_elem(const ProjArgs &a, int64_t i, bool pend, int deff, const double *gc,
                                         const double *gs, double (&v)[MC + 1]) {
+    const int nload = pend ? a.M : deff;
+    V col[MC];
     const V ax = ldro<V>(a.Ax, i);
+#pragma unroll
+    for (int k = 0; k < MC; ++k) col[k] = (k < nload) ? ldrw<V>(a.Bt + k * a.ld, i) : vzero(V());
     v[MC] = vdot(ax, ax, v[MC]);
     if (pend) {
-        // Givens sweep over B~ column pairs, columns streamed in registers (PAPER.md:285-288,
-        // App. A): new column k = c_k t + s_k B_{k+1}; t carries the rotated remainder.
-        V col[MC];
-#pragma unroll
-        for (int k = 0; k < MC; ++k)
-            if (k < a.M) col[k] = ldrw<V>(a.Bt + k * a.ld, i);
+        // Givens sweep over B~ column pairs streamed in registers (App. A
+        // P:1800-1815): new column k = c_k t + s_k B_{k+1}; t carries the rotated remainder.
         V t = col[0];
 #pragma unroll
         for (int k = 0; k < MC - 1; ++k) {
@@ -205,13 +245,12 @@ __device__ __forceinline__ void u1_elem(const ProjArgs &a, int64_t i, bool pend,
         }
     } else {
 #pragma unroll
-        for (int k = 0; k < MC; ++k)
-            if (k < deff) v[k] = vdot(ldrw<V>(a.Bt + k * a.ld, i), ax, v[k]);
+        for (int k = 0; k < MC; ++k) v[k] = vdot(col[k], ax, v[k]);
     }
 }
 
 template <int MC, int VEC>
-__global__ void __launch_bounds__(THREADS) k_u1(ProjArgs a) {
+__global__ void __launch_bounds__(THREADS, 1) k_u1(ProjArgs a) {
     typedef typename VT<VEC>::T V;
     __shared__ double sh[(THREADS / 32) * (MC + 1)];
     __shared__ double s_gc[MAXM], s_gs[MAXM];
@@ -255,27 +294,10 @@ __global__ void __launch_bounds__(THREADS) k_u1(ProjArgs a) {
 }
 
 // ------------------------------------------------------------------ update pass 2
-template <int MC, class V>
-__device__ __forceinline__ void u2_elem(const ProjArgs &a, int64_t i, int deff, const double *c1,
-                                        double (&v)[MC + 1]) {
-    const V ax = ldro<V>(a.Ax, i);
-    V col[MC];
-#pragma unroll
-    for (int k = 0; k < MC; ++k)
-        if (k < deff) col[k] = ldro<V>(a.Bt + k * a.ld, i);
-    V b1 = ax;  // b1 = Ax - B~ c1, formed in registers only
-#pragma unroll
-    for (int k = 0; k < MC; ++k)
-        if (k < deff) b1 = vaxpy(-c1[k], col[k], b1);
-#pragma unroll
-    for (int k = 0; k < MC; ++k)
-        if (k < deff) v[k] = vdot(col[k], b1, v[k]);
-    v[MC] = vdot(b1, b1, v[MC]);
-}
-
 template <int MC, int VEC>
-__global__ void __launch_bounds__(THREADS) k_u2(ProjArgs a) {
+__global__ void __launch_bounds__(THREADS, 1) k_u2(ProjArgs a) {
     typedef typename VT<VEC>::T V;
+    constexpr int U = Unroll<MC>::U;
     __shared__ double sh[(THREADS / 32) * (MC + 1)];
     __shared__ double s_c1[MAXM];
     Ctrl *c = a.ctrl;
@@ -292,9 +314,38 @@ __global__ void __launch_bounds__(THREADS) k_u2(ProjArgs a) {
     for (int k = 0; k <= MC; ++k) v[k] = 0.0;
     const int64_t nv = a.N / VEC;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nv; i += stride)
-        u2_elem<MC, V>(a, i, deff, c1, v);
-    if (VEC == 2 && (a.N & 1) && blockIdx.x == 0 && threadIdx.x == 0) u2_elem<MC, double>(a, a.N - 1, deff, c1, v);
+    for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i0 < nv; i0 += U * stride) {
+        V ax[U], col[U][MC];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int64_t i = i0 + u * stride;
+            const bool ok = i < nv;
+            ax[u] = ok ? ldro<V>(a.Ax, i) : vzero(V());
+#pragma unroll
+            for (int k = 0; k < MC; ++k) col[u][k] = (ok && k < deff) ? ldro<V>(a.Bt + k * a.ld, i) : vzero(V());
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            V b1 = ax[u];  // b1 = Ax - B~ c1, formed in registers only
+#pragma unroll
+            for (int k = 0; k < MC; ++k) b1 = vaxpy(-c1[k], col[u][k], b1);
+#pragma unroll
+            for (int k = 0; k < MC; ++k) v[k] = vdot(col[u][k], b1, v[k]);
+            v[MC] = vdot(b1, b1, v[MC]);
+        }
+    }
+    if (VEC == 2 && (a.N & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
+        const int64_t i = a.N - 1;
+        double col[MC];
+#pragma unroll
+        for (int k = 0; k < MC; ++k) col[k] = (k < deff) ? a.Bt[k * a.ld + i] : 0.0;
+        double b1 = a.Ax[i];
+#pragma unroll
+        for (int k = 0; k < MC; ++k) b1 = fma(-c1[k], col[k], b1);
+#pragma unroll
+        for (int k = 0; k < MC; ++k) v[k] = fma(col[k], b1, v[k]);
+        v[MC] = fma(b1, b1, v[MC]);
+    }
     if (block_partials_ticket<MC + 1>(v, deff, true, a.blk, &c->ticket[ST_U2], sh)) {
         final_reduce(deff, true, a.blk, a.part + ST_U2 * PS);
         if (threadIdx.x == 0) c->ticket[ST_U2] = 0;
@@ -304,44 +355,52 @@ __global__ void __launch_bounds__(THREADS) k_u2(ProjArgs a) {
 // ------------------------------------------------------------------ update store (+ X~ downdate)
 template <int MC, class V>
 __device__ __forceinline__ void u3_elem(const ProjArgs &a, int64_t i, int deff, bool rotX, bool adm,
-                                        double inv, const double *cc, const double *gc, const double *gs) {
-    V b2 = vzero(V());
+                                        double inv, const double *c1, const double *c2, const double *gc,
+                                        const double *gs) {
+    // loads first: Ax, x, B~ (admitted), X~ (rotated and/or combined)
+    const int nB = adm ? deff : 0;
+    const int nX = rotX ? a.M : nB;
+    V ax = vzero(V()), xv = vzero(V());
+    V bc[MC], xc[MC];
     if (adm) {
-        const V ax = ldro<V>(a.Ax, i);
-        V col[MC];
-#pragma unroll
-        for (int k = 0; k < MC; ++k)
-            if (k < deff) col[k] = ldro<V>(a.Bt + k * a.ld, i);
-        b2 = ax;  // b~ = Ax - B~ (c1 + c2)
-#pragma unroll
-        for (int k = 0; k < MC; ++k)
-            if (k < deff) b2 = vaxpy(-cc[k], col[k], b2);
+        ax = ldro<V>(a.Ax, i);
+        xv = ldro<V>(a.x, i);
     }
-    V xt = vzero(V());
-    if (adm) xt = ldro<V>(a.x, i);
-    if (rotX) {
-        V col[MC];
 #pragma unroll
-        for (int k = 0; k < MC; ++k)
-            if (k < a.M) col[k] = ldrw<V>(a.Xt + k * a.ld, i);
-        V t = col[0];
+    for (int k = 0; k < MC; ++k) bc[k] = (k < nB) ? ldro<V>(a.Bt + k * a.ld, i) : vzero(V());
+#pragma unroll
+    for (int k = 0; k < MC; ++k) xc[k] = (k < nX) ? ldrw<V>(a.Xt + k * a.ld, i) : vzero(V());
+    // The two Gram-Schmidt corrections are applied SEPARATELY, as in the listing:
+    // b~ = (Ax - B~ c1) - B~ c2, x~ = (x - X~ c1) - X~ c2.  Folding them into c1+c2 first would
+    // round away c2 (|c2| ~ u |c1|) and undo the re-orthogonalisation (AMB-7).
+    V b1 = ax, s2 = vzero(V());
+#pragma unroll
+    for (int k = 0; k < MC; ++k) b1 = vaxpy(-c1[k], bc[k], b1);  // same FMA order as k_u2
+#pragma unroll
+    for (int k = 0; k < MC; ++k) s2 = vaxpy(c2[k], bc[k], s2);
+    V xt = xv, t2 = vzero(V());
+    if (rotX) {
+        V t = xc[0];
 #pragma unroll
         for (int k = 0; k < MC - 1; ++k) {
             if (k < a.M - 1) {
                 V nk;
-                vrot(gc[k], gs[k], t, col[k + 1], nk);
+                vrot(gc[k], gs[k], t, xc[k + 1], nk);
                 stv<V>(a.Xt + k * a.ld, i, nk);
-                if (adm) xt = vaxpy(-cc[k], nk, xt);
+                xt = vaxpy(-c1[k], nk, xt);
+                t2 = vaxpy(c2[k], nk, t2);
             }
         }
-    } else if (adm) {
+    } else {
 #pragma unroll
-        for (int k = 0; k < MC; ++k)
-            if (k < deff) xt = vaxpy(-cc[k], ldrw<V>(a.Xt + k * a.ld, i), xt);
+        for (int k = 0; k < MC; ++k) {
+            xt = vaxpy(-c1[k], xc[k], xt);
+            t2 = vaxpy(c2[k], xc[k], t2);
+        }
     }
     if (adm) {  // "B~_{d+1} <- b~/||b~||, X~_{d+1} <- x~/||b~||" (rhsUpdateSpace)
-        stv<V>(a.Bt + deff * a.ld, i, vscale(inv, b2));
-        stv<V>(a.Xt + deff * a.ld, i, vscale(inv, xt));
+        stv<V>(a.Bt + deff * a.ld, i, vscale(inv, vaxpy(-1.0, s2, b1)));
+        stv<V>(a.Xt + deff * a.ld, i, vscale(inv, vaxpy(-1.0, t2, xt)));
     }
 }
 
@@ -381,9 +440,9 @@ __device__ void givens_plan(Ctrl *c, int M, double *H) {
 }
 
 template <int MC, int VEC>
-__global__ void __launch_bounds__(THREADS) k_u3(ProjArgs a) {
+__global__ void __launch_bounds__(THREADS, 1) k_u3(ProjArgs a) {
     typedef typename VT<VEC>::T V;
-    __shared__ double s_cc[MAXM], s_gc[MAXM], s_gs[MAXM];
+    __shared__ double s_c1[MAXM], s_c2[MAXM], s_gc[MAXM], s_gs[MAXM];
     __shared__ double s_nb, s_nAx;
     __shared__ int s_adm;
     __shared__ unsigned s_ticket;
@@ -394,7 +453,8 @@ __global__ void __launch_bounds__(THREADS) k_u3(ProjArgs a) {
     const double *g1 = a.gath + ST_U1 * a.G * PS;
     const double *g2 = a.gath + ST_U2 * a.G * PS;
     if (threadIdx.x < deff) {
-        s_cc[threadIdx.x] = rank_sum(g1, a.G, threadIdx.x) + rank_sum(g2, a.G, threadIdx.x);
+        s_c1[threadIdx.x] = rank_sum(g1, a.G, threadIdx.x);
+        s_c2[threadIdx.x] = rank_sum(g2, a.G, threadIdx.x);
     }
     if (rotX && threadIdx.x < M - 1) {
         s_gc[threadIdx.x] = c->gc[threadIdx.x];
@@ -421,10 +481,11 @@ __global__ void __launch_bounds__(THREADS) k_u3(ProjArgs a) {
     __syncthreads();
     const bool adm = s_adm != 0;
     const double inv = adm ? 1.0 / s_nb : 0.0;
-    double cc[MC], gc[MC], gs[MC];
+    double c1[MC], c2[MC], gc[MC], gs[MC];
 #pragma unroll
     for (int k = 0; k < MC; ++k) {
-        cc[k] = (k < deff) ? s_cc[k] : 0.0;
+        c1[k] = (k < deff) ? s_c1[k] : 0.0;
+        c2[k] = (k < deff) ? s_c2[k] : 0.0;
         gc[k] = (rotX && k < M - 1) ? s_gc[k] : 1.0;
         gs[k] = (rotX && k < M - 1) ? s_gs[k] : 0.0;
     }
@@ -432,9 +493,9 @@ __global__ void __launch_bounds__(THREADS) k_u3(ProjArgs a) {
         const int64_t nv = a.N / VEC;
         const int64_t stride = (int64_t)gridDim.x * blockDim.x;
         for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nv; i += stride)
-            u3_elem<MC, V>(a, i, deff, rotX, adm, inv, cc, gc, gs);
+            u3_elem<MC, V>(a, i, deff, rotX, adm, inv, c1, c2, gc, gs);
         if (VEC == 2 && (a.N & 1) && blockIdx.x == 0 && threadIdx.x == 0)
-            u3_elem<MC, double>(a, a.N - 1, deff, rotX, adm, inv, cc, gc, gs);
+            u3_elem<MC, double>(a, a.N - 1, deff, rotX, adm, inv, c1, c2, gc, gs);
     }
     __threadfence();
     __syncthreads();
@@ -445,7 +506,7 @@ __global__ void __launch_bounds__(THREADS) k_u3(ProjArgs a) {
     const int dnew = deff + (adm ? 1 : 0);
     if (a.method == M_PROJ_QR && adm) {  // R_{1:d,d+1} = c1 + c2, R_{d+1,d+1} = ||b~||
         for (int k = threadIdx.x; k < MAXM; k += blockDim.x)
-            c->R[k + deff * MAXM] = (k < deff) ? s_cc[k] : (k == deff ? s_nb : 0.0);
+            c->R[k + deff * MAXM] = (k < deff) ? s_c1[k] + s_c2[k] : (k == deff ? s_nb : 0.0);
     }
     __syncthreads();
     if (threadIdx.x == 0) {

@@ -12,4 +12,4 @@ if [ -n "${NCU}" ]; then
      python bench.py --steps 3 --warmup 10 --e2e-steps 1 --no-cpu-baseline > gpurun_out/ncu_bench.log 2>&1
   echo "ncu rc=$?" >> gpurun_out/ncu_bench.log
 fi
-tail -3 gpurun_out/pytest_gpu.log gpurun_out/smoke.log gpurun_out/bench.log
+for f in pytest_gpu smoke bench; do tail -n 3 gpurun_out/$f.log; done
