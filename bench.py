@@ -65,7 +65,8 @@ def bytes_per_step(M: int, N: int):
     proj = (8 * M + 4) * vb  # form 2(M+1) + U1 2M + U2 M + U3 3M+2
     extrap = (M + 1) * vb + 2 * vb  # combine of M + write x0, push by copy
     per_kernel = {"form_dot": (M + 1) * vb, "form_combine": (M + 1) * vb, "u1": 2 * M * vb, "u2": M * vb,
-                  "u3": (3 * M + 2) * vb, "extrap": (M + 1) * vb, "copy": 2 * vb}
+                  "u3": (3 * M + 2) * vb, "extrap": (M + 1) * vb, "copy": 2 * vb,
+                  "form_fused": 2 * (M + 1) * vb, "update_fused": (6 * M + 2) * vb}
     return proj, extrap, per_kernel
 
 

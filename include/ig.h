@@ -89,6 +89,12 @@ int ig_set_stream(ig_t h, void *cuda_stream);
  * admitted iff ||b~|| > eps_rel * ||A x|| after the two Gram-Schmidt passes.  Default 1e-10. */
 int ig_set_admit_tol(ig_t h, double eps_rel);
 
+/* Projection kernel schedule.  fused = 1 (default): on a single rank each ig_form_guess /
+ * ig_update is ONE persistent cooperatively-launched kernel whose passes are separated by
+ * software grid barriers.  fused = 0, or any handle with an attached multi-rank communicator:
+ * one kernel per pass with the NCCL exchange of partial sums between them.  Same arithmetic. */
+int ig_set_schedule(ig_t h, int fused);
+
 /* ---------------------------------------------------------------- the hot path */
 
 /* Form the initial guess for A x = b.
@@ -175,7 +181,9 @@ enum ig_kernel {
     IG_K_U3 = 4,           /* X~ downdate + store       (paper: rhsUpdateSpace, ...)      */
     IG_K_EXTRAP = 5,       /* x0 = sum beta_i x_i       (paper: extrapKernel)             */
     IG_K_COPY = 6,         /* window push by copy                                        */
-    IG_NKERNELS = 7
+    IG_K_FORM_FUSED = 7,   /* persistent form: dots -> grid barrier -> combine           */
+    IG_K_UPDATE_FUSED = 8, /* persistent update: U1 -> barrier -> U2 -> barrier -> U3    */
+    IG_NKERNELS = 9
 };
 int ig_profile(ig_t h, int enable);
 int ig_profile_read(ig_t h, int kernel, double *total_ms, int64_t *launches);

@@ -30,6 +30,7 @@ from .ig import (  # noqa: F401
     ig_profile_read,
     ig_reset,
     ig_set_admit_tol,
+    ig_set_schedule,
     ig_set_stream,
     ig_total_launches,
     ig_update,

@@ -35,6 +35,7 @@ _SIGS = {
     "ig_last_error": (C.c_char_p, []),
     "ig_set_stream": (C.c_int, [_P, _P]),
     "ig_set_admit_tol": (C.c_int, [_P, C.c_double]),
+    "ig_set_schedule": (C.c_int, [_P, C.c_int]),
     "ig_form_guess": (C.c_int, [_P, _P, _P]),
     "ig_update": (C.c_int, [_P, _P, _P]),
     "ig_form_guess_host": (C.c_int, [_P, _P, _P]),
@@ -54,7 +55,7 @@ _SIGS = {
     "ig_profile_read": (C.c_int, [_P, C.c_int, _D, C.POINTER(C.c_int64)]),
 }
 
-KERNELS = ["form_dot", "form_combine", "u1", "u2", "u3", "extrap", "copy"]
+KERNELS = ["form_dot", "form_combine", "u1", "u2", "u3", "extrap", "copy", "form_fused", "update_fused"]
 
 _lib = None
 

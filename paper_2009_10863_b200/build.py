@@ -18,8 +18,8 @@ INCLUDE = os.path.join(ROOT, "include")
 BUILD = os.path.join(ROOT, "build", "libig")
 LIB = os.path.join(PKG, "libig.so")
 
-SOURCES = ["kern_proj.cu", "kern_extrap.cu", "coeffs.cpp", "api.cpp"]
-HEADERS = [os.path.join(CSRC, "ig_internal.h"), os.path.join(INCLUDE, "ig.h")]
+SOURCES = ["kern_proj.cu", "kern_fused.cu", "kern_extrap.cu", "coeffs.cpp", "api.cpp"]
+HEADERS = [os.path.join(CSRC, "ig_internal.h"), os.path.join(CSRC, "proj_common.cuh"), os.path.join(INCLUDE, "ig.h")]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xptxas", "-v", f"-I{INCLUDE}", f"-I{CSRC}"]
 

@@ -105,6 +105,7 @@ struct ig_ctx {
     Ctrl *ctrl = nullptr;
     double *blk = nullptr, *part = nullptr, *gath = nullptr;
     int G = 1;
+    bool fused = true;  // persistent fused kernels when G == 1 (ig_set_schedule)
     ig_comm_ctx *comm = nullptr;
     // extrapolation
     std::vector<std::vector<double>> table;  // table[f-1]: weights for f stored solutions
@@ -262,7 +263,7 @@ ig_t create_impl(int64_t N, int method, int m, int degree, void *storage, size_t
         h->Bt = h->slab;
         h->Xt = h->slab + (size_t)m * h->ld;
         bool ok = cudaMalloc(&h->ctrl, sizeof(Ctrl)) == cudaSuccess &&
-                  cudaMalloc(&h->blk, sizeof(double) * PS * MAXB) == cudaSuccess &&
+                  cudaMalloc(&h->blk, 2 * sizeof(double) * PS * MAXB) == cudaSuccess &&
                   cudaMalloc(&h->part, sizeof(double) * PS * NSTAGE) == cudaSuccess;
         if (!ok || cudaMemset(h->ctrl, 0, sizeof(Ctrl)) != cudaSuccess ||
             cudaMemset(h->part, 0, sizeof(double) * PS * NSTAGE) != cudaSuccess) {
@@ -331,6 +332,12 @@ int ig_set_stream(ig_t h, void *s) {
     return IG_OK;
 }
 
+int ig_set_schedule(ig_t h, int fused) {
+    if (!h) return set_err(IG_E_ARG, "NULL handle");
+    h->fused = fused != 0;
+    return IG_OK;
+}
+
 int ig_set_admit_tol(ig_t h, double eps) {
     if (!h || !(eps >= 0.0)) return set_err(IG_E_ARG, "bad handle or eps");
     h->eps = eps;
@@ -355,6 +362,12 @@ int ig_form_guess(ig_t h, const double *b, double *x0) {
         a.b = b;
         a.x0 = x0;
         const int vec = (al16(b) && al16(x0)) ? 2 : 1;
+        if (h->G == 1 && h->fused) {
+            Prof p(h, IG_K_FORM_FUSED);
+            CUDA_OK(launch_form_fused(a, vec, h->nsm, h->stream));
+            count(h, 1);
+            return IG_OK;
+        }
         {
             Prof p(h, IG_K_FORM_DOT);
             CUDA_OK(launch_form_dot(a, vec, h->nsm, h->stream));
@@ -400,6 +413,12 @@ int ig_update(ig_t h, const double *x, const double *Ax) {
         a.x = x;
         a.Ax = Ax;
         const int vec = (al16(x) && al16(Ax)) ? 2 : 1;
+        if (h->G == 1 && h->fused) {
+            Prof p(h, IG_K_UPDATE_FUSED);
+            CUDA_OK(launch_update_fused(a, vec, h->nsm, h->stream));
+            count(h, 1);
+            return IG_OK;
+        }
         {
             Prof p(h, IG_K_U1);
             CUDA_OK(launch_u1(a, vec, h->nsm, h->stream));

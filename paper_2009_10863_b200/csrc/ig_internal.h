@@ -27,6 +27,7 @@ struct Ctrl {
     int admitted;   // last update admitted its pair
     int last_rot;   // the last update applied a downdate (bytes accounting)
     unsigned ticket[NSTAGE];
+    unsigned bar, bar_exit;        // grid barrier / exit counters of the fused kernels
     double rho, nAx, nb;
     double gc[MAXM], gs[MAXM];      // Givens (c_i, s_i) of the pending downdate
     double R[MAXM * MAXM];          // R, column-major R(i,j) = R[i + j*MAXM]
@@ -68,6 +69,9 @@ cudaError_t launch_form_combine(const ProjArgs &a, int vec, int nsm, cudaStream_
 cudaError_t launch_u1(const ProjArgs &a, int vec, int nsm, cudaStream_t s);
 cudaError_t launch_u2(const ProjArgs &a, int vec, int nsm, cudaStream_t s);
 cudaError_t launch_u3(const ProjArgs &a, int vec, int nsm, cudaStream_t s);
+// Persistent fused kernels (single GPU): one cooperative launch per call.
+cudaError_t launch_form_fused(const ProjArgs &a, int vec, int nsm, cudaStream_t s);
+cudaError_t launch_update_fused(const ProjArgs &a, int vec, int nsm, cudaStream_t s);
 cudaError_t launch_extrap(const ExtrapArgs &a, int vec, int nsm, cudaStream_t s);
 cudaError_t launch_copy(double *dst, const double *src, int64_t N, int vec, int nsm, cudaStream_t s);
 

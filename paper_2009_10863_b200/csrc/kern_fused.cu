@@ -1,0 +1,244 @@
+// kern_fused.cu -- persistent, cooperatively launched projection kernels for a single GPU.
+//
+// One launch per library call instead of one per pass: the passes of Alg. 2
+// are separated by software grid barriers, and after each reduction EVERY CTA sums the block
+// partials in the same fixed order (bitwise-identical coefficients in all CTAs, no serial
+// last-block finish, no fp64 atomics).  This removes the per-kernel ramp-up/drain and launch
+// gaps that dominate at the C2 size (2M DOFs, ~25-70 us per pass).
+//
+//   k_form_fused   : [alpha = B~^T b] --barrier--> [x0 = X~ alpha]
+//   k_update_fused : [B~ downdate + c1, ||Ax||^2] --barrier--> [c2, ||b1||^2] --barrier-->
+//                    [X~ downdate + x~, b~, admission, new columns] --exit--> control block
+// The element arithmetic is the same device code as the one-kernel-per-pass path
+// (proj_common.cuh), which stays in use when partial sums must cross ranks (G > 1).
+#include "proj_common.cuh"
+
+namespace ig {
+
+// Second block-partial buffer so that a fast CTA's pass-2 partials never overwrite pass-1
+// partials a slow CTA is still reading.
+constexpr int BLK2 = PS * MAXB;
+
+template <int MC, int VEC>
+__global__ void __launch_bounds__(THREADS, 1) k_form_fused(ProjArgs a) {
+    typedef typename VT<VEC>::T V;
+    constexpr int U = Unroll<MC>::U;
+    __shared__ double sh[(THREADS / 32) * (MC + 1)];
+    __shared__ double s_red[PS];
+    Ctrl *c = a.ctrl;
+    const int d = c->d;
+    if (d == 0) return;  // uniform: x0 stays the caller's fallback
+    const int64_t nv = a.N / VEC;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    const int64_t i_first = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    // ---- pass 1: alpha = B~^T b
+    double v[MC + 1];
+#pragma unroll
+    for (int k = 0; k <= MC; ++k) v[k] = 0.0;
+    for (int64_t i0 = i_first; i0 < nv; i0 += U * stride) {
+        V bv[U], col[U][MC];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int64_t i = i0 + u * stride;
+            const bool ok = i < nv;
+            bv[u] = ok ? ldro<V>(a.b, i) : vzero(V());
+#pragma unroll
+            for (int k = 0; k < MC; ++k) col[u][k] = (ok && k < d) ? ldro<V>(a.Bt + k * a.ld, i) : vzero(V());
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+#pragma unroll
+            for (int k = 0; k < MC; ++k) v[k] = vdot(col[u][k], bv[u], v[k]);
+    }
+    if (VEC == 2 && (a.N & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
+        const int64_t i = a.N - 1;
+        const double bv = a.b[i];
+#pragma unroll
+        for (int k = 0; k < MC; ++k)
+            if (k < d) v[k] = fma(a.Bt[k * a.ld + i], bv, v[k]);
+    }
+    block_partials_store<MC + 1>(v, d, false, a.blk, sh);
+    grid_barrier(&c->bar, 1);
+    reduce_all_blocks(d, false, a.blk, s_red);
+    double al[MC];
+#pragma unroll
+    for (int k = 0; k < MC; ++k) al[k] = (k < d) ? s_red[k] : 0.0;
+    // ---- pass 2: x0 = X~ alpha (b fully consumed before the barrier: x0 may alias b)
+    for (int64_t i0 = i_first; i0 < nv; i0 += U * stride) {
+        V col[U][MC];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int64_t i = i0 + u * stride;
+#pragma unroll
+            for (int k = 0; k < MC; ++k) col[u][k] = (i < nv && k < d) ? ldro<V>(a.Xt + k * a.ld, i) : vzero(V());
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int64_t i = i0 + u * stride;
+            V acc = vzero(V());
+#pragma unroll
+            for (int k = 0; k < MC; ++k) acc = vaxpy(al[k], col[u][k], acc);
+            if (i < nv) stv<V>(a.x0, i, acc);
+        }
+    }
+    if (VEC == 2 && (a.N & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
+        const int64_t i = a.N - 1;
+        double acc = 0.0;
+#pragma unroll
+        for (int k = 0; k < MC; ++k)
+            if (k < d) acc = fma(al[k], a.Xt[k * a.ld + i], acc);
+        a.x0[i] = acc;
+    }
+    if (grid_exit(&c->bar, &c->bar_exit) && threadIdx.x < d) a.part[ST_FORM * PS + threadIdx.x] = s_red[threadIdx.x];
+}
+
+template <int MC, int VEC>
+__global__ void __launch_bounds__(THREADS, 1) k_update_fused(ProjArgs a) {
+    typedef typename VT<VEC>::T V;
+    __shared__ double sh[(THREADS / 32) * (MC + 1)];
+    __shared__ double s_r1[PS], s_r2[PS];
+    __shared__ double s_gc[MAXM], s_gs[MAXM];
+    __shared__ double s_nb, s_nAx;
+    __shared__ int s_adm;
+    __shared__ double s_H[MAXM * MAXM];
+    Ctrl *c = a.ctrl;
+    const int d = c->d, M = a.M;
+    const bool pend = c->pending != 0;
+    const bool restart = (a.method == M_PROJ_CLASSIC) && (d >= M);  // Alg. 1 restart
+    const int deff = pend ? M - 1 : (restart ? 0 : d);
+    if (pend && threadIdx.x < M - 1) {
+        s_gc[threadIdx.x] = c->gc[threadIdx.x];
+        s_gs[threadIdx.x] = c->gs[threadIdx.x];
+    }
+    __syncthreads();
+    double gc[MC], gs[MC];
+#pragma unroll
+    for (int k = 0; k < MC; ++k) {
+        gc[k] = (pend && k < M - 1) ? s_gc[k] : 1.0;
+        gs[k] = (pend && k < M - 1) ? s_gs[k] : 0.0;
+    }
+    const int64_t nv = a.N / VEC;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    const int64_t i_first = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const bool tail = VEC == 2 && (a.N & 1) && blockIdx.x == 0 && threadIdx.x == 0;
+    // ---- pass 1: [Givens rotation of B~] + c1 = B~^T Ax, ||Ax||^2
+    double v[MC + 1];
+#pragma unroll
+    for (int k = 0; k <= MC; ++k) v[k] = 0.0;
+    for (int64_t i = i_first; i < nv; i += stride) u1_elem<MC, V>(a, i, pend, deff, gc, gs, v);
+    if (tail) u1_elem<MC, double>(a, a.N - 1, pend, deff, gc, gs, v);
+    block_partials_store<MC + 1>(v, deff, true, a.blk, sh);
+    grid_barrier(&c->bar, 1);
+    reduce_all_blocks(deff, true, a.blk, s_r1);
+    double c1[MC];
+#pragma unroll
+    for (int k = 0; k < MC; ++k) c1[k] = (k < deff) ? s_r1[k] : 0.0;
+    // ---- pass 2: b1 = Ax - B~ c1 (registers), c2 = B~^T b1, ||b1||^2
+    if (deff > 0) {
+#pragma unroll
+        for (int k = 0; k <= MC; ++k) v[k] = 0.0;
+        for (int64_t i = i_first; i < nv; i += stride) u2_elem<MC, V>(a, i, deff, c1, v);
+        if (tail) u2_elem<MC, double>(a, a.N - 1, deff, c1, v);
+        block_partials_store<MC + 1>(v, deff, true, a.blk + BLK2, sh);
+    }
+    grid_barrier(&c->bar, 2);
+    if (deff > 0) reduce_all_blocks(deff, true, a.blk + BLK2, s_r2);
+    if (threadIdx.x == 0) {
+        const double nAx2 = s_r1[NORM];
+        double nb2;
+        if (deff > 0) {
+            double c2sq = 0.0;
+            for (int k = 0; k < deff; ++k) c2sq = fma(s_r2[k], s_r2[k], c2sq);
+            nb2 = s_r2[NORM] - c2sq;  // ||b~2||^2 = ||b~1||^2 - ||c2||^2 (B~ orthonormal)
+        } else {
+            nb2 = nAx2;  // d = 0: b~ = Ax
+        }
+        const double nb = sqrt(fmax(nb2, 0.0)), nAx = sqrt(nAx2);
+        s_nb = nb;
+        s_nAx = nAx;
+        s_adm = (deff > 0) ? (nb > a.eps * nAx) : (nAx > 0.0);  // AMB-3 / AMB-6
+    }
+    __syncthreads();
+    const bool adm = s_adm != 0;
+    const double inv = adm ? 1.0 / s_nb : 0.0;
+    double c2[MC];
+#pragma unroll
+    for (int k = 0; k < MC; ++k) c2[k] = (k < deff) ? s_r2[k] : 0.0;
+    // ---- pass 3: [Givens rotation of X~] + store the admitted pair
+    if (adm || pend) {
+        for (int64_t i = i_first; i < nv; i += stride) u3_elem<MC, V>(a, i, deff, pend, adm, inv, c1, c2, gc, gs);
+        if (tail) u3_elem<MC, double>(a, a.N - 1, deff, pend, adm, inv, c1, c2, gc, gs);
+    }
+    // ---- epilogue (last CTA out): control block, R, next downdate's Givens
+    if (!grid_exit(&c->bar, &c->bar_exit)) return;
+    if (pend)
+        for (int idx = threadIdx.x; idx < MAXM * MAXM; idx += blockDim.x) c->R[idx] = c->Rdn[idx];
+    __syncthreads();
+    const int dnew = deff + (adm ? 1 : 0);
+    if (a.method == M_PROJ_QR && adm) {  // R_{1:d,d+1} = c1 + c2, R_{d+1,d+1} = ||b~||
+        for (int k = threadIdx.x; k < MAXM; k += blockDim.x)
+            c->R[k + deff * MAXM] = (k < deff) ? s_r1[k] + s_r2[k] : (k == deff ? s_nb : 0.0);
+    }
+    if (threadIdx.x < PS) {
+        a.part[ST_U1 * PS + threadIdx.x] = s_r1[threadIdx.x];
+        a.part[ST_U2 * PS + threadIdx.x] = (deff > 0) ? s_r2[threadIdx.x] : 0.0;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        c->d = dnew;
+        c->deff = deff;
+        c->pending = 0;
+        c->admitted = adm ? 1 : 0;
+        c->nb = s_nb;
+        c->nAx = s_nAx;
+        c->rho = (s_nAx > 0.0) ? s_nb / s_nAx : 0.0;
+        c->last_rot = pend ? 1 : 0;
+        c->rotX = 0;
+    }
+    __syncthreads();
+    if (a.method == M_PROJ_QR && dnew == M && threadIdx.x < 32) givens_plan(c, M, s_H);
+}
+
+// ------------------------------------------------------------------ cooperative launchers
+template <class K> static cudaError_t coop_launch(K kern, const ProjArgs &a, int nsm, cudaStream_t s) {
+    static_assert(sizeof(ProjArgs) < 4096, "kernel parameters");
+    int occ = 0;
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, THREADS, 0);
+    if (e != cudaSuccess) return e;
+    if (occ < 1) return cudaErrorInvalidConfiguration;
+    if (occ > 4) occ = 4;
+    int grid = nsm * occ;
+    if (grid > MAXB) grid = MAXB;
+    ProjArgs args = a;
+    void *params[] = {&args};
+    return cudaLaunchCooperativeKernel((const void *)kern, dim3(grid), dim3(THREADS), params, 0, s);
+}
+
+static int mcb(int M) { return M <= 1 ? 1 : M <= 2 ? 2 : M <= 4 ? 4 : M <= 8 ? 8 : M <= 16 ? 16 : 32; }
+
+#define IG_FUSED_DISPATCH(KERNEL, ARGS, VEC_IN, NSM, STREAM)                                        \
+    do {                                                                                            \
+        const int mc = mcb((ARGS).M);                                                               \
+        const bool v2 = ((VEC_IN) == 2) && mc <= 8;                                                 \
+        switch (mc) {                                                                               \
+        case 1: return v2 ? coop_launch(KERNEL<1, 2>, ARGS, NSM, STREAM)                            \
+                          : coop_launch(KERNEL<1, 1>, ARGS, NSM, STREAM);                           \
+        case 2: return v2 ? coop_launch(KERNEL<2, 2>, ARGS, NSM, STREAM)                            \
+                          : coop_launch(KERNEL<2, 1>, ARGS, NSM, STREAM);                           \
+        case 4: return v2 ? coop_launch(KERNEL<4, 2>, ARGS, NSM, STREAM)                            \
+                          : coop_launch(KERNEL<4, 1>, ARGS, NSM, STREAM);                           \
+        case 8: return v2 ? coop_launch(KERNEL<8, 2>, ARGS, NSM, STREAM)                            \
+                          : coop_launch(KERNEL<8, 1>, ARGS, NSM, STREAM);                           \
+        case 16: return coop_launch(KERNEL<16, 1>, ARGS, NSM, STREAM);                              \
+        default: return coop_launch(KERNEL<32, 1>, ARGS, NSM, STREAM);                              \
+        }                                                                                           \
+    } while (0)
+
+cudaError_t launch_form_fused(const ProjArgs &a, int vec, int nsm, cudaStream_t s) {
+    IG_FUSED_DISPATCH(k_form_fused, a, vec, nsm, s);
+}
+cudaError_t launch_update_fused(const ProjArgs &a, int vec, int nsm, cudaStream_t s) {
+    IG_FUSED_DISPATCH(k_update_fused, a, vec, nsm, s);
+}
+
+}  // namespace ig

@@ -15,126 +15,9 @@
 // in warp order -> block partials -> the LAST block (atomic ticket) sums them in block order.
 // No fp64 atomics.  With G ranks the per-rank partials are all-gathered (NCCL, host-enqueued
 // between kernels) and every consumer sums them in rank order.
-#include "ig_internal.h"
+#include "proj_common.cuh"
 
 namespace ig {
-
-template <int VEC> struct VT;
-template <> struct VT<1> { typedef double T; };
-template <> struct VT<2> { typedef double2 T; };
-
-__device__ __forceinline__ double vzero(double) { return 0.0; }
-__device__ __forceinline__ double2 vzero(double2) { return make_double2(0.0, 0.0); }
-__device__ __forceinline__ double vdot(double a, double b, double acc) { return fma(a, b, acc); }
-__device__ __forceinline__ double vdot(double2 a, double2 b, double acc) {
-    return fma(a.y, b.y, fma(a.x, b.x, acc));
-}
-// y + s*a
-__device__ __forceinline__ double vaxpy(double s, double a, double y) { return fma(s, a, y); }
-__device__ __forceinline__ double2 vaxpy(double s, double2 a, double2 y) {
-    return make_double2(fma(s, a.x, y.x), fma(s, a.y, y.y));
-}
-__device__ __forceinline__ double vscale(double s, double a) { return s * a; }
-__device__ __forceinline__ double2 vscale(double s, double2 a) { return make_double2(s * a.x, s * a.y); }
-// (out, t) <- (c t + s n, -s t + c n): one Givens rotation of a column pair
-__device__ __forceinline__ void vrot(double c, double s, double &t, double n, double &out) {
-    out = c * t + s * n;
-    t = -s * t + c * n;
-}
-__device__ __forceinline__ void vrot(double c, double s, double2 &t, double2 n, double2 &out) {
-    vrot(c, s, t.x, n.x, out.x);
-    vrot(c, s, t.y, n.y, out.y);
-}
-
-template <class V> __device__ __forceinline__ V ldro(const double *base, int64_t i) {
-    return __ldg(reinterpret_cast<const V *>(base) + i);
-}
-template <class V> __device__ __forceinline__ V ldrw(const double *base, int64_t i) {
-    return reinterpret_cast<const V *>(base)[i];
-}
-template <class V> __device__ __forceinline__ void stv(double *base, int64_t i, V v) {
-    reinterpret_cast<V *>(base)[i] = v;
-}
-
-__device__ __forceinline__ double warp_sum(double v) {
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    return v;
-}
-
-// Block-reduce NV = MC+1 per-thread values (value MC is a squared norm, slot NORM), write this
-// block's partials to blk[slot*MAXB + blockIdx], and take a ticket.  Returns true in the block
-// that arrived last (it then owns the final, block-ordered reduction).
-template <int NV>
-__device__ __forceinline__ bool block_partials_ticket(const double (&v)[NV], int nc, bool norm, double *blk,
-                                                      unsigned *ticket, double *sh) {
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
-#pragma unroll
-    for (int k = 0; k < NV; ++k) {
-        const bool act = (k < NV - 1) ? (k < nc) : norm;  // warp-uniform
-        if (act) {
-            const double s = warp_sum(v[k]);
-            if (lane == 0) sh[w * NV + k] = s;
-        }
-    }
-    __syncthreads();
-    for (int k = threadIdx.x; k < NV; k += blockDim.x) {
-        const bool act = (k < NV - 1) ? (k < nc) : norm;
-        if (act) {
-            double s = 0.0;
-            for (int j = 0; j < nw; ++j) s += sh[j * NV + k];
-            blk[((k < NV - 1) ? k : NORM) * MAXB + blockIdx.x] = s;
-        }
-    }
-    __threadfence();
-    __syncthreads();
-    __shared__ unsigned s_ticket;
-    if (threadIdx.x == 0) s_ticket = atomicAdd(ticket, 1u);
-    __syncthreads();
-    const bool last = (s_ticket == gridDim.x - 1);
-    if (last) __threadfence();
-    return last;
-}
-
-// Last block: out[k] = sum over blocks of blk[k][*] in a fixed order: lane l owns blocks
-// l, l+32, ... accumulated 8-way (8 independent loads in flight), then a fixed xor tree.
-__device__ __forceinline__ void final_reduce(int nc, bool norm, const double *blk, double *out) {
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    const int nb = gridDim.x;
-    for (int k = w; k < PS; k += nw) {
-        const bool act = (k < MAXM) ? (k < nc) : norm;
-        if (!act) continue;
-        const double *row = blk + k * MAXB;
-        double s[8];
-#pragma unroll
-        for (int u = 0; u < 8; ++u) s[u] = 0.0;
-        int b = lane;
-        for (; b + 7 * 32 < nb; b += 8 * 32) {
-#pragma unroll
-            for (int u = 0; u < 8; ++u) s[u] += __ldcg(row + b + u * 32);
-        }
-        for (int u = 0; b < nb; b += 32, ++u) s[u] += __ldcg(row + b);
-        double t = ((s[0] + s[1]) + (s[2] + s[3])) + ((s[4] + s[5]) + (s[6] + s[7]));
-        t = warp_sum(t);
-        if (lane == 0) out[k] = t;
-    }
-}
-
-// Rank-ordered sum of the gathered partials of one stage.
-__device__ __forceinline__ double rank_sum(const double *g, int G, int k) {
-    double s = g[k];
-    for (int r = 1; r < G; ++r) s += g[r * PS + k];
-    return s;
-}
-
-// All streaming loops follow one pattern: every load of a trip is issued before any
-// arithmetic consumes it (`col[]` arrays), and the kernels are compiled with
-// __launch_bounds__(THREADS, 1) so ptxas keeps them grouped instead of interleaving loads with
-// their DFMAs to save registers (which cut memory-level parallelism to ~2 loads per thread).
-// Streams with few vectors process U strided elements per trip for more bytes in flight.
-template <int MC> struct Unroll {
-    static constexpr int U = MC <= 2 ? 4 : (MC <= 4 ? 2 : 1);
-};
 
 // ------------------------------------------------------------------ form: alpha = B~^T b
 template <int MC, int VEC>
@@ -221,34 +104,6 @@ __global__ void __launch_bounds__(THREADS, 1) k_form_combine(ProjArgs a) {
 }
 
 // ------------------------------------------------------------------ update pass 1 (+ B~ downdate)
-template <int MC, class V>
-__device__ __forceinline__ void u1_elem(const ProjArgs &a, int64_t i, bool pend, int deff, const double *gc,
-                                        const double *gs, double (&v)[MC + 1]) {
-    const int nload = pend ? a.M : deff;
-    V col[MC];
-    const V ax = ldro<V>(a.Ax, i);
-#pragma unroll
-    for (int k = 0; k < MC; ++k) col[k] = (k < nload) ? ldrw<V>(a.Bt + k * a.ld, i) : vzero(V());
-    v[MC] = vdot(ax, ax, v[MC]);
-    if (pend) {
-        // Givens sweep over B~ column pairs streamed in registers (App. A
-        // P:1800-1815): new column k = c_k t + s_k B_{k+1}; t carries the rotated remainder.
-        V t = col[0];
-#pragma unroll
-        for (int k = 0; k < MC - 1; ++k) {
-            if (k < a.M - 1) {
-                V nk;
-                vrot(gc[k], gs[k], t, col[k + 1], nk);
-                stv<V>(a.Bt + k * a.ld, i, nk);
-                v[k] = vdot(nk, ax, v[k]);
-            }
-        }
-    } else {
-#pragma unroll
-        for (int k = 0; k < MC; ++k) v[k] = vdot(col[k], ax, v[k]);
-    }
-}
-
 template <int MC, int VEC>
 __global__ void __launch_bounds__(THREADS, 1) k_u1(ProjArgs a) {
     typedef typename VT<VEC>::T V;
@@ -353,92 +208,6 @@ __global__ void __launch_bounds__(THREADS, 1) k_u2(ProjArgs a) {
 }
 
 // ------------------------------------------------------------------ update store (+ X~ downdate)
-template <int MC, class V>
-__device__ __forceinline__ void u3_elem(const ProjArgs &a, int64_t i, int deff, bool rotX, bool adm,
-                                        double inv, const double *c1, const double *c2, const double *gc,
-                                        const double *gs) {
-    // loads first: Ax, x, B~ (admitted), X~ (rotated and/or combined)
-    const int nB = adm ? deff : 0;
-    const int nX = rotX ? a.M : nB;
-    V ax = vzero(V()), xv = vzero(V());
-    V bc[MC], xc[MC];
-    if (adm) {
-        ax = ldro<V>(a.Ax, i);
-        xv = ldro<V>(a.x, i);
-    }
-#pragma unroll
-    for (int k = 0; k < MC; ++k) bc[k] = (k < nB) ? ldro<V>(a.Bt + k * a.ld, i) : vzero(V());
-#pragma unroll
-    for (int k = 0; k < MC; ++k) xc[k] = (k < nX) ? ldrw<V>(a.Xt + k * a.ld, i) : vzero(V());
-    // The two Gram-Schmidt corrections are applied SEPARATELY, as in the listing:
-    // b~ = (Ax - B~ c1) - B~ c2, x~ = (x - X~ c1) - X~ c2.  Folding them into c1+c2 first would
-    // round away c2 (|c2| ~ u |c1|) and undo the re-orthogonalisation (AMB-7).
-    V b1 = ax, s2 = vzero(V());
-#pragma unroll
-    for (int k = 0; k < MC; ++k) b1 = vaxpy(-c1[k], bc[k], b1);  // same FMA order as k_u2
-#pragma unroll
-    for (int k = 0; k < MC; ++k) s2 = vaxpy(c2[k], bc[k], s2);
-    V xt = xv, t2 = vzero(V());
-    if (rotX) {
-        V t = xc[0];
-#pragma unroll
-        for (int k = 0; k < MC - 1; ++k) {
-            if (k < a.M - 1) {
-                V nk;
-                vrot(gc[k], gs[k], t, xc[k + 1], nk);
-                stv<V>(a.Xt + k * a.ld, i, nk);
-                xt = vaxpy(-c1[k], nk, xt);
-                t2 = vaxpy(c2[k], nk, t2);
-            }
-        }
-    } else {
-#pragma unroll
-        for (int k = 0; k < MC; ++k) {
-            xt = vaxpy(-c1[k], xc[k], xt);
-            t2 = vaxpy(c2[k], xc[k], t2);
-        }
-    }
-    if (adm) {  // "B~_{d+1} <- b~/||b~||, X~_{d+1} <- x~/||b~||" (rhsUpdateSpace)
-        stv<V>(a.Bt + deff * a.ld, i, vscale(inv, vaxpy(-1.0, s2, b1)));
-        stv<V>(a.Xt + deff * a.ld, i, vscale(inv, vaxpy(-1.0, t2, xt)));
-    }
-}
-
-// One warp: Givens parameters of the next downdate from R (AMB-2 reading of P:279-290):
-// H = R_{:,2:M}; for i: a = H_ii, b = H_{i+1,i}, r = hypot(a,b), c = a/r, s = b/r; rotate rows.
-__device__ void givens_plan(Ctrl *c, int M, double *H) {
-    const int lane = threadIdx.x & 31;
-    for (int idx = lane; idx < MAXM * MAXM; idx += 32) {
-        const int i = idx / MAXM, j = idx % MAXM;
-        H[idx] = (i < M && j < M - 1) ? c->R[i + (j + 1) * MAXM] : 0.0;
-    }
-    __syncwarp();
-    for (int i = 0; i < M - 1; ++i) {
-        const double aa = H[i * MAXM + i], bb = H[(i + 1) * MAXM + i];
-        const double r = hypot(aa, bb);
-        const double cs = (r == 0.0) ? 1.0 : aa / r;
-        const double sn = (r == 0.0) ? 0.0 : bb / r;
-        __syncwarp();
-        const int j = lane;
-        if (j >= i && j < M - 1) {
-            const double hi = H[i * MAXM + j], hi1 = H[(i + 1) * MAXM + j];
-            H[i * MAXM + j] = cs * hi + sn * hi1;
-            H[(i + 1) * MAXM + j] = -sn * hi + cs * hi1;
-        }
-        if (lane == 0) {
-            c->gc[i] = cs;
-            c->gs[i] = sn;
-        }
-        __syncwarp();
-    }
-    for (int idx = lane; idx < MAXM * MAXM; idx += 32) {
-        const int i = idx % MAXM, j = idx / MAXM;  // column-major destination
-        c->Rdn[idx] = (i < M - 1 && j < M - 1 && i <= j) ? H[i * MAXM + j] : 0.0;
-    }
-    __syncwarp();
-    if (lane == 0) c->pending = 1;
-}
-
 template <int MC, int VEC>
 __global__ void __launch_bounds__(THREADS, 1) k_u3(ProjArgs a) {
     typedef typename VT<VEC>::T V;

@@ -83,6 +83,10 @@ def ig_set_admit_tol(h, eps: float) -> None:
     _check(lib().ig_set_admit_tol(h, float(eps)), "ig_set_admit_tol")
 
 
+def ig_set_schedule(h, fused: bool) -> None:
+    _check(lib().ig_set_schedule(h, 1 if fused else 0), "ig_set_schedule")
+
+
 def ig_set_stream(h, stream) -> None:
     _check(lib().ig_set_stream(h, C.c_void_p(stream.cuda_stream)), "ig_set_stream")
 
@@ -228,12 +232,14 @@ class InitialGuess:
     """One history space (one field).  Thin wrapper over an ig_t handle."""
 
     def __init__(self, N: int, method="proj_qr", m: int = 8, degree: int = 0, eps: float | None = None,
-                 comm=None, stream=None):
+                 comm=None, stream=None, fused: bool = True):
         self.N, self.m, self.degree = int(N), int(m), int(degree)
         self.method = METHODS[method] if isinstance(method, str) else int(method)
         self.h = ig_create(self.N, self.method, self.m, self.degree, stream)
         if eps is not None:
             ig_set_admit_tol(self.h, eps)
+        if not fused:
+            ig_set_schedule(self.h, False)
         if comm is not None:
             ig_attach_comm(self.h, comm)
 

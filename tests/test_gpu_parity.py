@@ -37,13 +37,13 @@ def _rel(a, b):
     return np.linalg.norm(a - b) / (nb if nb > 0 else 1.0)
 
 
-def run_proj_parity(g, M, steps, method="proj_qr", dt=1e-3, seq=None, misalign=False):
+def run_proj_parity(g, M, steps, method="proj_qr", dt=1e-3, seq=None, misalign=False, fused=True):
     from paper_2009_10863_b200 import InitialGuess
 
     seq = seq or _seq(g, steps, dt)
     N = g.N
     ora = (ProjQR if method == "proj_qr" else ProjClassic)(N, M)
-    ig = InitialGuess(N, method, M)
+    ig = InitialGuess(N, method, M, fused=fused)
     off = 1 if misalign else 0
     buf = torch.zeros(4 * (N + 1) + 8, dtype=torch.float64, device="cuda")
     views = [buf[i * (N + 1) + off:i * (N + 1) + off + N] for i in range(4)]
@@ -71,29 +71,39 @@ def run_proj_parity(g, M, steps, method="proj_qr", dt=1e-3, seq=None, misalign=F
     return worst
 
 
+# fused = persistent single-launch schedule (single-GPU default); split = one kernel per pass
+# (the schedule used with a multi-rank communicator).
+SCHEDULES = [pytest.param(True, id="fused"), pytest.param(False, id="split")]
+
+
+@pytest.mark.parametrize("fused", SCHEDULES)
 @pytest.mark.parametrize("M", [1, 2, 3, 5, 8, 12, 16, 30])
-def test_proj_qr_open_loop_c1(M):
+def test_proj_qr_open_loop_c1(M, fused):
     # configs[0]: 2D 32x32 5-point Helmholtz, 40 steps
-    run_proj_parity(Grid(32, 2), M, 40)
+    run_proj_parity(Grid(32, 2), M, 40, fused=fused)
 
 
+@pytest.mark.parametrize("fused", SCHEDULES)
 @pytest.mark.parametrize("M", [4, 8])
-def test_proj_classic_open_loop_c1(M):
-    run_proj_parity(Grid(32, 2), M, 30, method="proj_classic")
+def test_proj_classic_open_loop_c1(M, fused):
+    run_proj_parity(Grid(32, 2), M, 30, method="proj_classic", fused=fused)
 
 
+@pytest.mark.parametrize("fused", SCHEDULES)
 @pytest.mark.parametrize("n,dim", [(31, 2), (23, 3), (1001, 1), (3, 1), (1, 1)])
-def test_proj_qr_ragged_sizes(n, dim):
-    run_proj_parity(Grid(n, dim), 8, 14, dt=1e-2)
+def test_proj_qr_ragged_sizes(n, dim, fused):
+    run_proj_parity(Grid(n, dim), 8, 14, dt=1e-2, fused=fused)
 
 
-def test_proj_qr_misaligned_vectors_take_scalar_path():
-    run_proj_parity(Grid(33, 2), 4, 12, misalign=True)
+@pytest.mark.parametrize("fused", SCHEDULES)
+def test_proj_qr_misaligned_vectors_take_scalar_path(fused):
+    run_proj_parity(Grid(33, 2), 4, 12, misalign=True, fused=fused)
 
 
-def test_proj_qr_many_blocks_3d():
-    # 64^3 = 262,144 DOFs: hundreds of blocks, exercises the block-ordered finish
-    run_proj_parity(Grid(64, 3), 8, 12)
+@pytest.mark.parametrize("fused", SCHEDULES)
+def test_proj_qr_many_blocks_3d(fused):
+    # 64^3 = 262,144 DOFs: hundreds of blocks, exercises the block-ordered reductions
+    run_proj_parity(Grid(64, 3), 8, 12, fused=fused)
 
 
 def test_proj_orthonormality_and_R_vs_oracle():
