@@ -288,6 +288,72 @@ __device__ __forceinline__ void u3_elem(const ProjArgs &a, int64_t i, int deff, 
     }
 }
 
+
+// U-way unrolled variants (U strided elements per trip, all loads of the trip first): more bytes
+// in flight per thread for the passes that stream only d+1 vectors.
+template <int MC, int U, class V>
+__device__ __forceinline__ void u1_trip(const ProjArgs &a, int64_t i0, int64_t stride, int64_t nv, bool pend,
+                                        int deff, const double *gc, const double *gs, double (&v)[MC + 1]) {
+    const int nload = pend ? a.M : deff;
+    V col[U][MC], ax[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+        const int64_t i = i0 + u * stride;
+        const bool ok = i < nv;
+        ax[u] = ok ? ldro<V>(a.Ax, i) : vzero(V());
+#pragma unroll
+        for (int k = 0; k < MC; ++k) col[u][k] = (ok && k < nload) ? ldrw<V>(a.Bt + k * a.ld, i) : vzero(V());
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+        const int64_t i = i0 + u * stride;
+        v[MC] = vdot(ax[u], ax[u], v[MC]);
+        if (pend) {
+            V t = col[u][0];
+#pragma unroll
+            for (int k = 0; k < MC - 1; ++k) {
+                if (k < a.M - 1) {
+                    V nk;
+                    vrot(gc[k], gs[k], t, col[u][k + 1], nk);
+                    if (i < nv) stv<V>(a.Bt + k * a.ld, i, nk);
+                    v[k] = vdot(nk, ax[u], v[k]);
+                }
+            }
+        } else {
+#pragma unroll
+            for (int k = 0; k < MC; ++k) v[k] = vdot(col[u][k], ax[u], v[k]);
+        }
+    }
+}
+
+template <int MC, int U, class V>
+__device__ __forceinline__ void u2_trip(const ProjArgs &a, int64_t i0, int64_t stride, int64_t nv, int deff,
+                                        const double *c1, double (&v)[MC + 1]) {
+    V col[U][MC], ax[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+        const int64_t i = i0 + u * stride;
+        const bool ok = i < nv;
+        ax[u] = ok ? ldro<V>(a.Ax, i) : vzero(V());
+#pragma unroll
+        for (int k = 0; k < MC; ++k) col[u][k] = (ok && k < deff) ? ldro<V>(a.Bt + k * a.ld, i) : vzero(V());
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+        V b1 = ax[u];
+#pragma unroll
+        for (int k = 0; k < MC; ++k) b1 = vaxpy(-c1[k], col[u][k], b1);
+#pragma unroll
+        for (int k = 0; k < MC; ++k) v[k] = vdot(col[u][k], b1, v[k]);
+        v[MC] = vdot(b1, b1, v[MC]);
+    }
+}
+
+// Unroll of the fused kernels' d+1-stream passes (registers are sized by the X~ pass anyway).
+template <int MC> struct FusedUnroll {
+    static constexpr int U = MC <= 4 ? 4 : (MC <= 8 ? 2 : 1);
+};
+
 // One warp: Givens parameters of the next downdate from R (AMB-2 reading of P:279-290):
 // H = R_{:,2:M}; for i: a = H_ii, b = H_{i+1,i}, r = hypot(a,b), c = a/r, s = b/r; rotate rows.
 static __device__ __noinline__ void givens_plan(Ctrl *c, int M, double *H) {
