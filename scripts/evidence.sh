@@ -10,7 +10,7 @@ timeout 600 python bench.py --impl reference ${BENCH_ARGS} > gpurun_out/bench_re
 # launch list: 4 steady steps (warm-up launches skipped), cold-cache serialised
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:'k_' -s 80 -c 16 --csv \
    --log-file gpurun_out/launches.csv python bench.py --steps 4 --warmup 40 --e2e-steps 1 --no-cpu-baseline > gpurun_out/ncu_launch.log 2>&1
-KREGEX="k_update_fused|k_form_fused|k_extrap|k_copy" SKIP=80 COUNT=4 bash scripts/ncu_full.sh
+KREGEX="k_update_fused|k_form_fused|k_extrap|k_copy" SKIP=40 COUNT=4 bash scripts/ncu_full.sh
 python scripts/summarize_ncu.py --launches gpurun_out/launches.csv --full gpurun_out/prof.ncu-rep --bench gpurun_out/bench.log --tag ${TAG} > gpurun_out/summary.log 2>&1
 cp -r profiles gpurun_out/profiles_new
 for f in pytest_gpu smoke bench bench_ref; do tail -n 2 gpurun_out/$f.log; done
