@@ -19,6 +19,121 @@ namespace ig {
 // partials a slow CTA is still reading.
 constexpr int BLK2 = PS * MAXB;
 
+// ------------------------------------------------------------------ trip = loads, then arithmetic
+// The first trip of the pass AFTER a grid barrier is loaded BEFORE the barrier (the addresses do
+// not depend on the reduction; each thread only reads rows it wrote itself in earlier passes), so
+// the barrier + all-CTA reduction bubble overlaps useful HBM traffic.
+
+template <int MC, int U, class V> struct XTrip {  // form pass 2: U strided elements of d X~ columns
+    V col[U][MC];
+};
+template <int MC, int U, class V>
+__device__ __forceinline__ void xtrip_load(XTrip<MC, U, V> &r, const ProjArgs &a, int64_t i0, int64_t stride,
+                                           int64_t nv, int d) {
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+        const int64_t i = i0 + u * stride;
+#pragma unroll
+        for (int k = 0; k < MC; ++k) r.col[u][k] = (i < nv && k < d) ? ldro<V>(a.Xt + k * a.ld, i) : vzero(V());
+    }
+}
+template <int MC, int U, class V>
+__device__ __forceinline__ void xtrip_store(const XTrip<MC, U, V> &r, const ProjArgs &a, int64_t i0, int64_t stride,
+                                            int64_t nv, const double *al) {
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+        const int64_t i = i0 + u * stride;
+        V acc = vzero(V());
+#pragma unroll
+        for (int k = 0; k < MC; ++k) acc = vaxpy(al[k], r.col[u][k], acc);
+        if (i < nv) stv<V>(a.x0, i, acc);
+    }
+}
+
+template <int MC, int U, class V> struct U2Trip {  // update pass 2
+    V ax[U];
+    V col[U][MC];
+};
+template <int MC, int U, class V>
+__device__ __forceinline__ void u2trip_load(U2Trip<MC, U, V> &r, const ProjArgs &a, int64_t i0, int64_t stride,
+                                            int64_t nv, int deff) {
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+        const int64_t i = i0 + u * stride;
+        const bool ok = i < nv;
+        r.ax[u] = ok ? ldro<V>(a.Ax, i) : vzero(V());
+#pragma unroll
+        for (int k = 0; k < MC; ++k) r.col[u][k] = (ok && k < deff) ? ldrw<V>(a.Bt + k * a.ld, i) : vzero(V());
+    }
+}
+template <int MC, int U, class V>
+__device__ __forceinline__ void u2trip_compute(const U2Trip<MC, U, V> &r, const double *c1, double (&v)[MC + 1]) {
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+        V b1 = r.ax[u];  // b1 = Ax - B~ c1 (registers only)
+#pragma unroll
+        for (int k = 0; k < MC; ++k) b1 = vaxpy(-c1[k], r.col[u][k], b1);
+#pragma unroll
+        for (int k = 0; k < MC; ++k) v[k] = vdot(r.col[u][k], b1, v[k]);
+        v[MC] = vdot(b1, b1, v[MC]);
+    }
+}
+
+template <int MC, class V> struct U3Trip {  // update pass 3 (one element)
+    V ax, xv;
+    V bc[MC], xc[MC];
+};
+// Loads assume the pair is admitted (the common case); if it is not, the prefetched B~/Ax/x
+// values of that one trip are simply unused.
+template <int MC, class V>
+__device__ __forceinline__ void u3trip_load(U3Trip<MC, V> &r, const ProjArgs &a, int64_t i, int64_t nv, int deff,
+                                            bool rotX, bool adm) {
+    const bool ok = i < nv;
+    const int nB = adm ? deff : 0;
+    const int nX = rotX ? a.M : nB;
+    r.ax = (ok && adm) ? ldro<V>(a.Ax, i) : vzero(V());
+    r.xv = (ok && adm) ? ldro<V>(a.x, i) : vzero(V());
+#pragma unroll
+    for (int k = 0; k < MC; ++k) r.bc[k] = (ok && k < nB) ? ldrw<V>(a.Bt + k * a.ld, i) : vzero(V());
+#pragma unroll
+    for (int k = 0; k < MC; ++k) r.xc[k] = (ok && k < nX) ? ldrw<V>(a.Xt + k * a.ld, i) : vzero(V());
+}
+template <int MC, class V>
+__device__ __forceinline__ void u3trip_store(const U3Trip<MC, V> &r, const ProjArgs &a, int64_t i, int deff,
+                                             bool rotX, bool adm, double inv, const double *c1, const double *c2,
+                                             const double *gc, const double *gs) {
+    // b~ = (Ax - B~ c1) - B~ c2 ; x~ = (x - X~ c1) - X~ c2 (separate corrections, DESIGN.md AMB-7)
+    V b1 = r.ax, s2 = vzero(V());
+#pragma unroll
+    for (int k = 0; k < MC; ++k) b1 = vaxpy(-c1[k], r.bc[k], b1);
+#pragma unroll
+    for (int k = 0; k < MC; ++k) s2 = vaxpy(c2[k], r.bc[k], s2);
+    V xt = r.xv, t2 = vzero(V());
+    if (rotX) {
+        V t = r.xc[0];
+#pragma unroll
+        for (int k = 0; k < MC - 1; ++k) {
+            if (k < a.M - 1) {
+                V nk;
+                vrot(gc[k], gs[k], t, r.xc[k + 1], nk);
+                stv<V>(a.Xt + k * a.ld, i, nk);
+                xt = vaxpy(-c1[k], nk, xt);
+                t2 = vaxpy(c2[k], nk, t2);
+            }
+        }
+    } else {
+#pragma unroll
+        for (int k = 0; k < MC; ++k) {
+            xt = vaxpy(-c1[k], r.xc[k], xt);
+            t2 = vaxpy(c2[k], r.xc[k], t2);
+        }
+    }
+    if (adm) {
+        stv<V>(a.Bt + deff * a.ld, i, vscale(inv, vaxpy(-1.0, s2, b1)));
+        stv<V>(a.Xt + deff * a.ld, i, vscale(inv, vaxpy(-1.0, t2, xt)));
+    }
+}
+
 template <int MC, int VEC>
 __global__ void __launch_bounds__(THREADS, 1) k_form_fused(ProjArgs a) {
     typedef typename VT<VEC>::T V;
@@ -57,29 +172,20 @@ __global__ void __launch_bounds__(THREADS, 1) k_form_fused(ProjArgs a) {
         for (int k = 0; k < MC; ++k)
             if (k < d) v[k] = fma(a.Bt[k * a.ld + i], bv, v[k]);
     }
+    XTrip<MC, U, V> pre;  // first trip of pass 2, in flight across the barrier
+    xtrip_load(pre, a, i_first, stride, nv, d);
     block_partials_store<MC + 1>(v, d, false, a.blk, sh);
     grid_barrier(&c->bar, 1);
-    reduce_all_blocks(d, false, a.blk, s_red);
+    reduce_all_blocks<MC>(d, false, a.blk, s_red);
     double al[MC];
 #pragma unroll
     for (int k = 0; k < MC; ++k) al[k] = (k < d) ? s_red[k] : 0.0;
     // ---- pass 2: x0 = X~ alpha (b fully consumed before the barrier: x0 may alias b)
-    for (int64_t i0 = i_first; i0 < nv; i0 += U * stride) {
-        V col[U][MC];
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-            const int64_t i = i0 + u * stride;
-#pragma unroll
-            for (int k = 0; k < MC; ++k) col[u][k] = (i < nv && k < d) ? ldro<V>(a.Xt + k * a.ld, i) : vzero(V());
-        }
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-            const int64_t i = i0 + u * stride;
-            V acc = vzero(V());
-#pragma unroll
-            for (int k = 0; k < MC; ++k) acc = vaxpy(al[k], col[u][k], acc);
-            if (i < nv) stv<V>(a.x0, i, acc);
-        }
+    xtrip_store(pre, a, i_first, stride, nv, al);
+    for (int64_t i0 = i_first + U * stride; i0 < nv; i0 += U * stride) {
+        XTrip<MC, U, V> r;
+        xtrip_load(r, a, i0, stride, nv, d);
+        xtrip_store(r, a, i0, stride, nv, al);
     }
     if (VEC == 2 && (a.N & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
         const int64_t i = a.N - 1;
@@ -95,6 +201,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_form_fused(ProjArgs a) {
 template <int MC, int VEC>
 __global__ void __launch_bounds__(THREADS, 1) k_update_fused(ProjArgs a) {
     typedef typename VT<VEC>::T V;
+    constexpr int U = FusedUnroll<MC>::U;
     __shared__ double sh[(THREADS / 32) * (MC + 1)];
     __shared__ double s_r1[PS], s_r2[PS];
     __shared__ double s_gc[MAXM], s_gs[MAXM];
@@ -125,12 +232,17 @@ __global__ void __launch_bounds__(THREADS, 1) k_update_fused(ProjArgs a) {
     double v[MC + 1];
 #pragma unroll
     for (int k = 0; k <= MC; ++k) v[k] = 0.0;
-    constexpr int U = FusedUnroll<MC>::U;
     for (int64_t i0 = i_first; i0 < nv; i0 += U * stride) u1_trip<MC, U, V>(a, i0, stride, nv, pend, deff, gc, gs, v);
     if (tail) u1_elem<MC, double>(a, a.N - 1, pend, deff, gc, gs, v);
+    // Serpentine order: pass 2 walks the vectors BACKWARDS, so it starts on the B~/Ax lines pass 1
+    // touched last (still in the 126 MB L2); pass 3 walks forwards again and starts on what pass 2
+    // touched last.  Same arithmetic per element, fewer HBM bytes per step.
+    const int64_t ntrip2 = (i_first < nv) ? (nv - i_first + U * stride - 1) / (U * stride) : 0;
+    U2Trip<MC, U, V> pre2;
+    if (deff > 0 && ntrip2 > 0) u2trip_load(pre2, a, i_first + (ntrip2 - 1) * U * stride, stride, nv, deff);
     block_partials_store<MC + 1>(v, deff, true, a.blk, sh);
     grid_barrier(&c->bar, 1);
-    reduce_all_blocks(deff, true, a.blk, s_r1);
+    reduce_all_blocks<MC>(deff, true, a.blk, s_r1);
     double c1[MC];
 #pragma unroll
     for (int k = 0; k < MC; ++k) c1[k] = (k < deff) ? s_r1[k] : 0.0;
@@ -138,18 +250,19 @@ __global__ void __launch_bounds__(THREADS, 1) k_update_fused(ProjArgs a) {
     if (deff > 0) {
 #pragma unroll
         for (int k = 0; k <= MC; ++k) v[k] = 0.0;
-        // Serpentine order: pass 2 walks the vectors BACKWARDS, so it starts on the B~/Ax lines
-        // pass 1 touched last (still in the 126 MB L2); pass 3 walks forwards again and starts on
-        // what pass 2 touched last.  Same arithmetic per element, fewer HBM bytes per step.
-        if (i_first < nv) {
-            const int64_t ntrip = (nv - i_first + U * stride - 1) / (U * stride);
-            for (int64_t t = ntrip - 1; t >= 0; --t) u2_trip<MC, U, V>(a, i_first + t * U * stride, stride, nv, deff, c1, v);
+        if (ntrip2 > 0) u2trip_compute(pre2, c1, v);
+        for (int64_t t = ntrip2 - 2; t >= 0; --t) {
+            U2Trip<MC, U, V> r;
+            u2trip_load(r, a, i_first + t * U * stride, stride, nv, deff);
+            u2trip_compute(r, c1, v);
         }
         if (tail) u2_elem<MC, double>(a, a.N - 1, deff, c1, v);
-        block_partials_store<MC + 1>(v, deff, true, a.blk + BLK2, sh);
     }
+    U3Trip<MC, V> pre3;  // first element of pass 3, in flight across barrier 2
+    u3trip_load(pre3, a, i_first, nv, deff, pend, true);
+    if (deff > 0) block_partials_store<MC + 1>(v, deff, true, a.blk + BLK2, sh);
     grid_barrier(&c->bar, 2);
-    if (deff > 0) reduce_all_blocks(deff, true, a.blk + BLK2, s_r2);
+    if (deff > 0) reduce_all_blocks<MC>(deff, true, a.blk + BLK2, s_r2);
     if (threadIdx.x == 0) {
         const double nAx2 = s_r1[NORM];
         double nb2;
@@ -173,7 +286,12 @@ __global__ void __launch_bounds__(THREADS, 1) k_update_fused(ProjArgs a) {
     for (int k = 0; k < MC; ++k) c2[k] = (k < deff) ? s_r2[k] : 0.0;
     // ---- pass 3: [Givens rotation of X~] + store the admitted pair
     if (adm || pend) {
-        for (int64_t i = i_first; i < nv; i += stride) u3_elem<MC, V>(a, i, deff, pend, adm, inv, c1, c2, gc, gs);
+        if (i_first < nv) u3trip_store(pre3, a, i_first, deff, pend, adm, inv, c1, c2, gc, gs);
+        for (int64_t i = i_first + stride; i < nv; i += stride) {
+            U3Trip<MC, V> r;
+            u3trip_load(r, a, i, nv, deff, pend, adm);
+            u3trip_store(r, a, i, deff, pend, adm, inv, c1, c2, gc, gs);
+        }
         if (tail) u3_elem<MC, double>(a, a.N - 1, deff, pend, adm, inv, c1, c2, gc, gs);
     }
     // ---- epilogue (last CTA out): control block, R, next downdate's Givens

@@ -55,7 +55,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_form_dot(ProjArgs a) {
             if (k < d) v[k] = fma(a.Bt[k * a.ld + i], bv, v[k]);
     }
     if (block_partials_ticket<MC + 1>(v, d, false, a.blk, &a.ctrl->ticket[ST_FORM], sh)) {
-        final_reduce(d, false, a.blk, a.part + ST_FORM * PS);
+        final_reduce<MC>(d, false, a.blk, a.part + ST_FORM * PS);
         if (threadIdx.x == 0) a.ctrl->ticket[ST_FORM] = 0;
     }
 }
@@ -135,7 +135,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_u1(ProjArgs a) {
     if (VEC == 2 && (a.N & 1) && blockIdx.x == 0 && threadIdx.x == 0)
         u1_elem<MC, double>(a, a.N - 1, pend, deff, gc, gs, v);
     if (block_partials_ticket<MC + 1>(v, deff, true, a.blk, &c->ticket[ST_U1], sh)) {
-        final_reduce(deff, true, a.blk, a.part + ST_U1 * PS);
+        final_reduce<MC>(deff, true, a.blk, a.part + ST_U1 * PS);
         if (pend)
             for (int idx = threadIdx.x; idx < MAXM * MAXM; idx += blockDim.x) c->R[idx] = c->Rdn[idx];
         if (threadIdx.x == 0) {
@@ -202,7 +202,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_u2(ProjArgs a) {
         v[MC] = fma(b1, b1, v[MC]);
     }
     if (block_partials_ticket<MC + 1>(v, deff, true, a.blk, &c->ticket[ST_U2], sh)) {
-        final_reduce(deff, true, a.blk, a.part + ST_U2 * PS);
+        final_reduce<MC>(deff, true, a.blk, a.part + ST_U2 * PS);
         if (threadIdx.x == 0) c->ticket[ST_U2] = 0;
     }
 }

@@ -82,30 +82,49 @@ __device__ __forceinline__ bool block_partials_ticket(const double (&v)[NV], int
     return last;
 }
 
-// Last block: out[k] = sum over blocks of blk[k][*] in a fixed order: lane l owns blocks
-// l, l+32, ... accumulated 8-way (8 independent loads in flight), then a fixed xor tree.
+// out[slot] = sum over the gridDim.x block partials of that slot, in a fixed order.  The MC+1
+// possible slots (coefficients 0..MC-1, the norm) are dealt to warps round-robin; lane l owns
+// blocks l, l+32, ...; each chunk issues all its loads (up to 8 blocks x JS slots) at once, so
+// <= 256 blocks cost one L2 round trip; then a fixed xor tree.  Deterministic for a given grid.
+template <int MC>
 __device__ __forceinline__ void final_reduce(int nc, bool norm, const double *blk, double *out) {
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    constexpr int NW = THREADS / 32;
+    constexpr int JS = (MC + 1 + NW - 1) / NW;
     const int nb = gridDim.x;
-    for (int k = w; k < PS; k += nw) {
-        const bool act = (k < MAXM) ? (k < nc) : norm;
-        if (!act) continue;
-        const double *row = blk + k * MAXB;
-        double s[8];
+    double s[JS][8];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) s[u] = 0.0;
-        int b = lane;
-        for (; b + 7 * 32 < nb; b += 8 * 32) {
+    for (int j = 0; j < JS; ++j)
 #pragma unroll
-            for (int u = 0; u < 8; ++u) s[u] += __ldcg(row + b + u * 32);
+        for (int u = 0; u < 8; ++u) s[j][u] = 0.0;
+    for (int base = lane; base < nb; base += 8 * 32) {
+        double t[JS][8];
+#pragma unroll
+        for (int j = 0; j < JS; ++j) {
+            const int q = w + j * NW;  // compact slot index: q < MC -> coefficient q, q == MC -> norm
+            const bool act = (q < MC) ? (q < nc) : (q == MC && norm);
+            const int k = (q < MC) ? q : NORM;
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int bb = base + u * 32;
+                t[j][u] = (act && bb < nb) ? __ldcg(blk + k * MAXB + bb) : 0.0;
+            }
         }
-        for (int u = 0; b < nb; b += 32, ++u) s[u] += __ldcg(row + b);
-        double t = ((s[0] + s[1]) + (s[2] + s[3])) + ((s[4] + s[5]) + (s[6] + s[7]));
+#pragma unroll
+        for (int j = 0; j < JS; ++j)
+#pragma unroll
+            for (int u = 0; u < 8; ++u) s[j][u] += t[j][u];
+    }
+#pragma unroll
+    for (int j = 0; j < JS; ++j) {
+        const int q = w + j * NW;
+        const bool act = (q < MC) ? (q < nc) : (q == MC && norm);
+        if (!act) continue;  // warp-uniform
+        double t = ((s[j][0] + s[j][1]) + (s[j][2] + s[j][3])) + ((s[j][4] + s[j][5]) + (s[j][6] + s[j][7]));
         t = warp_sum(t);
-        if (lane == 0) out[k] = t;
+        if (lane == 0) out[(q < MC) ? q : NORM] = t;
     }
 }
-
 
 // ------------------------------------------------------------------ persistent-kernel helpers
 // Block-reduce NV per-thread values and store this block's partials (no ticket).
@@ -173,8 +192,9 @@ __device__ __forceinline__ bool grid_exit(unsigned *ctr, unsigned *exit_ctr) {
 
 // Every CTA reduces all block partials of a stage in the same fixed order (so all CTAs hold
 // bitwise-identical sums) into out[slot] (shared memory).  Ends with __syncthreads().
+template <int MC>
 __device__ __forceinline__ void reduce_all_blocks(int nc, bool norm, const double *blk, double *out) {
-    final_reduce(nc, norm, blk, out);
+    final_reduce<MC>(nc, norm, blk, out);
     __syncthreads();
 }
 
