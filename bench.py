@@ -276,8 +276,10 @@ def run_ours(args, world, rank, local):
     l0 = ig_total_launches()
     with sampler:
         e0.record(stream)
+        th0 = time.perf_counter()
         for k in range(prefill + W, S):
             step(k)
+        host_us = (time.perf_counter() - th0) / K * 1e6  # host enqueue cost per step (async launches)
         e1.record(stream)
         torch.cuda.synchronize()
     barrier(world)
@@ -375,7 +377,7 @@ def run_ours(args, world, rank, local):
                           "parallelism": f"dof-shard{world}" if world > 1 else "single"},
                "gpu_launches": launches, "roofline": roofline, "kernels": kernels,
                "clocks": sampler.summary(), "e2e": e2e, "cpu_baseline": cpu,
-               "proj_state": {"d": st["d"], "rho_last": st["rho"]}}
+               "proj_state": {"d": st["d"], "rho_last": st["rho"]}, "host_enqueue_us_per_step": host_us}
         print(json.dumps(out), flush=True)
 
 

@@ -14,6 +14,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
+#include <unordered_map>
 #include <string>
 #include <vector>
 
@@ -41,6 +42,21 @@ static int set_err(int code, const char *fmt, ...) {
         if (e_ != cudaSuccess)                                                                 \
             return set_err(IG_E_CUDA, "%s: %s (%s:%d)", #expr, cudaGetErrorString(e_), __FILE__, __LINE__); \
     } while (0)
+
+int ig::cached_occupancy(const void *kernel) {
+    static std::mutex mu;
+    static std::unordered_map<const void *, int> cache;
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = cache.find(kernel);
+    if (it != cache.end()) return it->second;
+    int occ = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, THREADS, 0) != cudaSuccess) {
+        cudaGetLastError();
+        occ = 0;
+    }
+    cache[kernel] = occ;
+    return occ;
+}
 
 // ----------------------------------------------------------------------------- NCCL (dlopen)
 namespace {

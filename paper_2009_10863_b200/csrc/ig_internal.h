@@ -75,6 +75,10 @@ cudaError_t launch_update_fused(const ProjArgs &a, int vec, int nsm, cudaStream_
 cudaError_t launch_extrap(const ExtrapArgs &a, int vec, int nsm, cudaStream_t s);
 cudaError_t launch_copy(double *dst, const double *src, int64_t N, int vec, int nsm, cudaStream_t s);
 
+// Cached cudaOccupancyMaxActiveBlocksPerMultiprocessor(kernel, THREADS) (api.cpp); the query is
+// ~microseconds of host time, paid once per kernel instantiation instead of per launch.
+int cached_occupancy(const void *kernel);
+
 // Host weight builders (coeffs.cpp).
 // EXTRAP(m, M) least-squares weights, oldest first (Householder QR of the Legendre Vandermonde).
 int build_ls_weights(int m, int M, double *beta);

@@ -327,9 +327,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_update_fused(ProjArgs a) {
 // ------------------------------------------------------------------ cooperative launchers
 template <class K> static cudaError_t coop_launch(K kern, const ProjArgs &a, int nsm, cudaStream_t s) {
     static_assert(sizeof(ProjArgs) < 4096, "kernel parameters");
-    int occ = 0;
-    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, THREADS, 0);
-    if (e != cudaSuccess) return e;
+    int occ = cached_occupancy((const void *)kern);
     if (occ < 1) return cudaErrorInvalidConfiguration;
     if (occ > 4) occ = 4;
     int grid = nsm * occ;

@@ -293,8 +293,8 @@ __global__ void __launch_bounds__(THREADS, 1) k_u3(ProjArgs a) {
 
 // ------------------------------------------------------------------ launchers
 template <class K> static int grid_for(K kern, int64_t nv, int nsm) {
-    int occ = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, THREADS, 0) != cudaSuccess || occ < 1) occ = 1;
+    int occ = cached_occupancy((const void *)kern);
+    if (occ < 1) occ = 1;
     if (occ > 4) occ = 4;
     int64_t want = (nv + THREADS - 1) / THREADS;
     int64_t g = (int64_t)nsm * occ;
