@@ -59,13 +59,15 @@ def peak_hbm():
         return FALLBACK_HBM, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
-def bytes_per_step(M: int, N: int):
-    """Algorithmic fp64 traffic of one steady step."""
+def bytes_per_step(M: int, N: int, nnz: int | None = None):
+    """Algorithmic fp64 traffic of one steady step.  nnz = extrapolation weights
+    that are nonzero (only those solutions are streamed; M for a dense scheme)."""
     vb = 8 * N
+    nnz = M if nnz is None else nnz
     proj = (8 * M + 4) * vb  # form 2(M+1) + U1 2M + U2 M + U3 3M+2
-    extrap = (M + 1) * vb + 2 * vb  # combine of M + write x0, push by copy
+    extrap = (nnz + 1) * vb + 2 * vb  # combine of the nonzero-weight solutions + write x0, push by copy
     per_kernel = {"form_dot": (M + 1) * vb, "form_combine": (M + 1) * vb, "u1": 2 * M * vb, "u2": M * vb,
-                  "u3": (3 * M + 2) * vb, "extrap": (M + 1) * vb, "copy": 2 * vb,
+                  "u3": (3 * M + 2) * vb, "extrap": (nnz + 1) * vb, "copy": 2 * vb,
                   "form_fused": 2 * (M + 1) * vb, "update_fused": (6 * M + 2) * vb}
     return proj, extrap, per_kernel
 
@@ -194,7 +196,8 @@ def oracle_sample_run(n: int, M: int, degree: int, nz: int, steps: int, budget_s
         x_prev = x
         done += 1
         k += 1
-    pb, eb, _ = bytes_per_step(M, N)
+    nnz = int(np.count_nonzero(oe.weights()))
+    pb, eb, _ = bytes_per_step(M, N, nnz)
     return tot / max(done, 1), pb + eb, done, N
 
 
@@ -287,8 +290,11 @@ def run_ours(args, world, rank, local):
     t_ms = max_over_ranks(e0.elapsed_time(e1), world)
     st = hp.stats()
     fb, ub = hp.bytes()
-    pb, eb, per_kernel = bytes_per_step(M, N)
+    nnz = sum(1 for w in he.weights() if w != 0.0)
+    pb, eb, per_kernel = bytes_per_step(M, N, nnz)
     assert fb + ub == pb, f"library byte count {fb + ub} != analytic {pb}"
+    efb, eub = he.bytes()
+    assert efb + eub == eb, f"library extrapolation byte count {efb + eub} != analytic {eb}"
     assert st["admitted"] == 1
 
     step_bytes = pb + eb
@@ -371,7 +377,8 @@ def run_ours(args, world, rank, local):
                "config": {"workload": f"C2 3D {n}^3 7-point Helmholtz manufactured sequence, QR({M}) + EXTRAP({p},{M})",
                           "dofs_per_gpu": N, "history_m": M, "degree": p, "prefill_steps": prefill,
                           "bytes_per_step_per_gpu": step_bytes,
-                          "bytes_model": "QR (8M+4)*8N + EXTRAP (M+1)*8N + push copy 2*8N",
+                          "bytes_model": "QR (8M+4)*8N + EXTRAP (nnz(beta)+1)*8N + push copy 2*8N",
+                          "extrap_nnz": nnz,
                           "l2": f"fresh inputs every step; per-step working set "
                                 f"{(2 * M + M + 5) * 8 * N / 1e9:.2f} GB > L2 126 MB",
                           "parallelism": f"dof-shard{world}" if world > 1 else "single"},

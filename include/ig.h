@@ -149,7 +149,8 @@ int ig_history_dim(ig_t h, int *d);
 int ig_weights(ig_t h, int f, double *beta, int *len);
 
 /* Algorithmic bytes (8 bytes per fp64 value loaded or stored) of the last ig_form_guess and
- * the last ig_update, per the fused schedule in DESIGN.md "Bytes".  Syncs (reads d). */
+ * the last ig_update, per the fused schedule in DESIGN.md §7.  Extrapolation counts the solutions
+ * actually streamed (nonzero weights) + the x0 write.  Syncs (reads d). */
 int ig_bytes(ig_t h, int64_t *form_bytes, int64_t *update_bytes);
 
 typedef struct ig_stats {

@@ -30,3 +30,4 @@ from .extrap_ls import (  # noqa: F401
     warmup_weights,
     lebesgue,
 )
+from .sparse import ExtrapSparse, cpqr_pivots_exact, sparse_weights, sparse_weights_exact  # noqa: F401

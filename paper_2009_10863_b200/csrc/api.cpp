@@ -405,12 +405,20 @@ int ig_form_guess(ig_t h, const double *b, double *x0) {
     a.f = f;
     a.N = h->N;
     a.x0 = x0;
+    // Only nonzero weights are streamed (exact zeros contribute exactly nothing): SPEXTRAP reads
+    // its m+1 selected solutions (Table 1: (m+2)N), LS skips e.g. beta_4 = 0 of EXTRAP(3,8).
     bool aligned = al16(x0);
+    int nz = 0;
     for (int j = 0; j < f; ++j) {
-        a.src[j] = h->slots[slot_index(h, j)];
-        a.beta[j] = h->table[f - 1][j];
-        aligned = aligned && al16(a.src[j]);
+        const double bj = h->table[f - 1][j];
+        if (bj == 0.0) continue;
+        a.src[nz] = h->slots[slot_index(h, j)];
+        a.beta[nz] = bj;
+        aligned = aligned && al16(a.src[nz]);
+        ++nz;
     }
+    a.f = nz;
+    h->last_form_f = nz;
     {
         Prof p(h, IG_K_EXTRAP);
         CUDA_OK(launch_extrap(a, aligned ? 2 : 1, h->nsm, h->stream));

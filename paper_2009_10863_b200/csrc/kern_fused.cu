@@ -11,6 +11,8 @@
 //                    [X~ downdate + x~, b~, admission, new columns] --exit--> control block
 // The element arithmetic is the same device code as the one-kernel-per-pass path
 // (proj_common.cuh), which stays in use when partial sums must cross ranks (G > 1).
+#include <type_traits>
+
 #include "proj_common.cuh"
 
 namespace ig {
@@ -66,8 +68,8 @@ __device__ __forceinline__ void u2trip_load(U2Trip<MC, U, V> &r, const ProjArgs 
         for (int k = 0; k < MC; ++k) r.col[u][k] = (ok && k < deff) ? ldrw<V>(a.Bt + k * a.ld, i) : vzero(V());
     }
 }
-template <int MC, int U, class V>
-__device__ __forceinline__ void u2trip_compute(const U2Trip<MC, U, V> &r, const double *c1, double (&v)[MC + 1]) {
+template <int MC, int U, class V, class CP>
+__device__ __forceinline__ void u2trip_compute(const U2Trip<MC, U, V> &r, CP c1, double (&v)[MC + 1]) {
 #pragma unroll
     for (int u = 0; u < U; ++u) {
         V b1 = r.ax[u];  // b1 = Ax - B~ c1 (registers only)
@@ -79,58 +81,67 @@ __device__ __forceinline__ void u2trip_compute(const U2Trip<MC, U, V> &r, const 
     }
 }
 
-template <int MC, class V> struct U3Trip {  // update pass 3 (one element)
-    V ax, xv;
-    V bc[MC], xc[MC];
+template <int MC, int U, class V> struct U3Trip {  // update pass 3: U strided elements
+    V ax[U], xv[U];
+    V bc[U][MC], xc[U][MC];
 };
 // Loads assume the pair is admitted (the common case); if it is not, the prefetched B~/Ax/x
 // values of that one trip are simply unused.
-template <int MC, class V>
-__device__ __forceinline__ void u3trip_load(U3Trip<MC, V> &r, const ProjArgs &a, int64_t i, int64_t nv, int deff,
-                                            bool rotX, bool adm) {
-    const bool ok = i < nv;
+template <int MC, int U, class V>
+__device__ __forceinline__ void u3trip_load(U3Trip<MC, U, V> &r, const ProjArgs &a, int64_t i0, int64_t stride,
+                                            int64_t nv, int deff, bool rotX, bool adm) {
     const int nB = adm ? deff : 0;
     const int nX = rotX ? a.M : nB;
-    r.ax = (ok && adm) ? ldro<V>(a.Ax, i) : vzero(V());
-    r.xv = (ok && adm) ? ldro<V>(a.x, i) : vzero(V());
 #pragma unroll
-    for (int k = 0; k < MC; ++k) r.bc[k] = (ok && k < nB) ? ldrw<V>(a.Bt + k * a.ld, i) : vzero(V());
+    for (int u = 0; u < U; ++u) {
+        const int64_t i = i0 + u * stride;
+        const bool ok = i < nv;
+        r.ax[u] = (ok && adm) ? ldro<V>(a.Ax, i) : vzero(V());
+        r.xv[u] = (ok && adm) ? ldro<V>(a.x, i) : vzero(V());
 #pragma unroll
-    for (int k = 0; k < MC; ++k) r.xc[k] = (ok && k < nX) ? ldrw<V>(a.Xt + k * a.ld, i) : vzero(V());
+        for (int k = 0; k < MC; ++k) r.bc[u][k] = (ok && k < nB) ? ldrw<V>(a.Bt + k * a.ld, i) : vzero(V());
+#pragma unroll
+        for (int k = 0; k < MC; ++k) r.xc[u][k] = (ok && k < nX) ? ldrw<V>(a.Xt + k * a.ld, i) : vzero(V());
+    }
 }
-template <int MC, class V>
-__device__ __forceinline__ void u3trip_store(const U3Trip<MC, V> &r, const ProjArgs &a, int64_t i, int deff,
-                                             bool rotX, bool adm, double inv, const double *c1, const double *c2,
-                                             const double *gc, const double *gs) {
-    // b~ = (Ax - B~ c1) - B~ c2 ; x~ = (x - X~ c1) - X~ c2 (separate corrections, DESIGN.md AMB-7)
-    V b1 = r.ax, s2 = vzero(V());
+template <int MC, int U, class V, class CP>
+__device__ __forceinline__ void u3trip_store(const U3Trip<MC, U, V> &r, const ProjArgs &a, int64_t i0,
+                                             int64_t stride, int64_t nv, int deff, bool rotX, bool adm, double inv,
+                                             CP c1, CP c2, CP gc, CP gs) {
 #pragma unroll
-    for (int k = 0; k < MC; ++k) b1 = vaxpy(-c1[k], r.bc[k], b1);
+    for (int u = 0; u < U; ++u) {
+        const int64_t i = i0 + u * stride;
+        if (i >= nv) break;
+        // b~ = (Ax - B~ c1) - B~ c2 ; x~ = (x - X~ c1) - X~ c2 (separate corrections, DESIGN.md AMB-7)
+        V b1 = r.ax[u], s2 = vzero(V());
 #pragma unroll
-    for (int k = 0; k < MC; ++k) s2 = vaxpy(c2[k], r.bc[k], s2);
-    V xt = r.xv, t2 = vzero(V());
-    if (rotX) {
-        V t = r.xc[0];
+        for (int k = 0; k < MC; ++k) b1 = vaxpy(-c1[k], r.bc[u][k], b1);
 #pragma unroll
-        for (int k = 0; k < MC - 1; ++k) {
-            if (k < a.M - 1) {
-                V nk;
-                vrot(gc[k], gs[k], t, r.xc[k + 1], nk);
-                stv<V>(a.Xt + k * a.ld, i, nk);
-                xt = vaxpy(-c1[k], nk, xt);
-                t2 = vaxpy(c2[k], nk, t2);
+        for (int k = 0; k < MC; ++k) s2 = vaxpy(c2[k], r.bc[u][k], s2);
+        V xt = r.xv[u], t2 = vzero(V());
+        if (rotX) {
+            V t = r.xc[u][0];
+#pragma unroll
+            for (int k = 0; k < MC - 1; ++k) {
+                if (k < a.M - 1) {
+                    V nk;
+                    vrot(gc[k], gs[k], t, r.xc[u][k + 1], nk);
+                    stv<V>(a.Xt + k * a.ld, i, nk);
+                    xt = vaxpy(-c1[k], nk, xt);
+                    t2 = vaxpy(c2[k], nk, t2);
+                }
+            }
+        } else {
+#pragma unroll
+            for (int k = 0; k < MC; ++k) {
+                xt = vaxpy(-c1[k], r.xc[u][k], xt);
+                t2 = vaxpy(c2[k], r.xc[u][k], t2);
             }
         }
-    } else {
-#pragma unroll
-        for (int k = 0; k < MC; ++k) {
-            xt = vaxpy(-c1[k], r.xc[k], xt);
-            t2 = vaxpy(c2[k], r.xc[k], t2);
+        if (adm) {
+            stv<V>(a.Bt + deff * a.ld, i, vscale(inv, vaxpy(-1.0, s2, b1)));
+            stv<V>(a.Xt + deff * a.ld, i, vscale(inv, vaxpy(-1.0, t2, xt)));
         }
-    }
-    if (adm) {
-        stv<V>(a.Bt + deff * a.ld, i, vscale(inv, vaxpy(-1.0, s2, b1)));
-        stv<V>(a.Xt + deff * a.ld, i, vscale(inv, vaxpy(-1.0, t2, xt)));
     }
 }
 
@@ -204,7 +215,9 @@ __global__ void __launch_bounds__(THREADS, 1) k_update_fused(ProjArgs a) {
     constexpr int U = FusedUnroll<MC>::U;
     __shared__ double sh[(THREADS / 32) * (MC + 1)];
     __shared__ double s_r1[PS], s_r2[PS];
-    __shared__ double s_gc[MAXM], s_gs[MAXM];
+    __shared__ double s_gc[MAXM], s_gs[MAXM], s_c1[MAXM], s_c2[MAXM];
+    constexpr bool SMC = FusedUnroll<MC>::SMEM_COEF;
+    constexpr int U3 = FusedUnroll<MC>::U3;
     __shared__ double s_nb, s_nAx;
     __shared__ int s_adm;
     __shared__ double s_H[MAXM * MAXM];
@@ -213,17 +226,25 @@ __global__ void __launch_bounds__(THREADS, 1) k_update_fused(ProjArgs a) {
     const bool pend = c->pending != 0;
     const bool restart = (a.method == M_PROJ_CLASSIC) && (d >= M);  // Alg. 1 restart
     const int deff = pend ? M - 1 : (restart ? 0 : d);
-    if (pend && threadIdx.x < M - 1) {
-        s_gc[threadIdx.x] = c->gc[threadIdx.x];
-        s_gs[threadIdx.x] = c->gs[threadIdx.x];
+    if (threadIdx.x < MAXM) {
+        const bool rot = pend && threadIdx.x < M - 1;
+        s_gc[threadIdx.x] = rot ? c->gc[threadIdx.x] : 1.0;
+        s_gs[threadIdx.x] = rot ? c->gs[threadIdx.x] : 0.0;
     }
     __syncthreads();
-    double gc[MC], gs[MC];
+    double gcr[SMC ? 1 : MC], gsr[SMC ? 1 : MC], c1r[SMC ? 1 : MC], c2r[SMC ? 1 : MC];
+    if constexpr (!SMC) {
 #pragma unroll
-    for (int k = 0; k < MC; ++k) {
-        gc[k] = (pend && k < M - 1) ? s_gc[k] : 1.0;
-        gs[k] = (pend && k < M - 1) ? s_gs[k] : 0.0;
+        for (int k = 0; k < MC; ++k) {
+            gcr[k] = s_gc[k];
+            gsr[k] = s_gs[k];
+        }
     }
+    typedef typename std::conditional<SMC, const volatile double *, const double *>::type CP;
+    const CP gc = SMC ? (CP)s_gc : (CP)gcr;
+    const CP gs = SMC ? (CP)s_gs : (CP)gsr;
+    const CP c1 = SMC ? (CP)s_c1 : (CP)c1r;
+    const CP c2 = SMC ? (CP)s_c2 : (CP)c2r;
     const int64_t nv = a.N / VEC;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     const int64_t i_first = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -233,7 +254,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_update_fused(ProjArgs a) {
 #pragma unroll
     for (int k = 0; k <= MC; ++k) v[k] = 0.0;
     for (int64_t i0 = i_first; i0 < nv; i0 += U * stride) u1_trip<MC, U, V>(a, i0, stride, nv, pend, deff, gc, gs, v);
-    if (tail) u1_elem<MC, double>(a, a.N - 1, pend, deff, gc, gs, v);
+    if (tail) u1_trip<MC, 1, double>(a, a.N - 1, 1, a.N, pend, deff, gc, gs, v);
     // Serpentine order: pass 2 walks the vectors BACKWARDS, so it starts on the B~/Ax lines pass 1
     // touched last (still in the 126 MB L2); pass 3 walks forwards again and starts on what pass 2
     // touched last.  Same arithmetic per element, fewer HBM bytes per step.
@@ -243,9 +264,12 @@ __global__ void __launch_bounds__(THREADS, 1) k_update_fused(ProjArgs a) {
     block_partials_store<MC + 1>(v, deff, true, a.blk, sh);
     grid_barrier(&c->bar, 1);
     reduce_all_blocks<MC>(deff, true, a.blk, s_r1);
-    double c1[MC];
+    if (threadIdx.x < MAXM) s_c1[threadIdx.x] = (threadIdx.x < deff) ? s_r1[threadIdx.x] : 0.0;
+    __syncthreads();
+    if constexpr (!SMC) {
 #pragma unroll
-    for (int k = 0; k < MC; ++k) c1[k] = (k < deff) ? s_r1[k] : 0.0;
+        for (int k = 0; k < MC; ++k) c1r[k] = s_c1[k];
+    }
     // ---- pass 2: b1 = Ax - B~ c1 (registers), c2 = B~^T b1, ||b1||^2
     if (deff > 0) {
 #pragma unroll
@@ -256,10 +280,14 @@ __global__ void __launch_bounds__(THREADS, 1) k_update_fused(ProjArgs a) {
             u2trip_load(r, a, i_first + t * U * stride, stride, nv, deff);
             u2trip_compute(r, c1, v);
         }
-        if (tail) u2_elem<MC, double>(a, a.N - 1, deff, c1, v);
+        if (tail) {
+            U2Trip<MC, 1, double> r;
+            u2trip_load(r, a, a.N - 1, 1, a.N, deff);
+            u2trip_compute(r, c1, v);
+        }
     }
-    U3Trip<MC, V> pre3;  // first element of pass 3, in flight across barrier 2
-    u3trip_load(pre3, a, i_first, nv, deff, pend, true);
+    U3Trip<MC, U3, V> pre3;  // first trip of pass 3, in flight across barrier 2
+    u3trip_load(pre3, a, i_first, stride, nv, deff, pend, true);
     if (deff > 0) block_partials_store<MC + 1>(v, deff, true, a.blk + BLK2, sh);
     grid_barrier(&c->bar, 2);
     if (deff > 0) reduce_all_blocks<MC>(deff, true, a.blk + BLK2, s_r2);
@@ -281,18 +309,25 @@ __global__ void __launch_bounds__(THREADS, 1) k_update_fused(ProjArgs a) {
     __syncthreads();
     const bool adm = s_adm != 0;
     const double inv = adm ? 1.0 / s_nb : 0.0;
-    double c2[MC];
+    if (threadIdx.x < MAXM) s_c2[threadIdx.x] = (deff > 0 && threadIdx.x < deff) ? s_r2[threadIdx.x] : 0.0;
+    __syncthreads();
+    if constexpr (!SMC) {
 #pragma unroll
-    for (int k = 0; k < MC; ++k) c2[k] = (k < deff) ? s_r2[k] : 0.0;
+        for (int k = 0; k < MC; ++k) c2r[k] = s_c2[k];
+    }
     // ---- pass 3: [Givens rotation of X~] + store the admitted pair
     if (adm || pend) {
-        if (i_first < nv) u3trip_store(pre3, a, i_first, deff, pend, adm, inv, c1, c2, gc, gs);
-        for (int64_t i = i_first + stride; i < nv; i += stride) {
-            U3Trip<MC, V> r;
-            u3trip_load(r, a, i, nv, deff, pend, adm);
-            u3trip_store(r, a, i, deff, pend, adm, inv, c1, c2, gc, gs);
+        u3trip_store(pre3, a, i_first, stride, nv, deff, pend, adm, inv, c1, c2, gc, gs);
+        for (int64_t i0 = i_first + U3 * stride; i0 < nv; i0 += U3 * stride) {
+            U3Trip<MC, U3, V> r;
+            u3trip_load(r, a, i0, stride, nv, deff, pend, adm);
+            u3trip_store(r, a, i0, stride, nv, deff, pend, adm, inv, c1, c2, gc, gs);
         }
-        if (tail) u3_elem<MC, double>(a, a.N - 1, deff, pend, adm, inv, c1, c2, gc, gs);
+        if (tail) {
+            U3Trip<MC, 1, double> r;
+            u3trip_load(r, a, a.N - 1, 1, a.N, deff, pend, adm);
+            u3trip_store(r, a, a.N - 1, 1, a.N, deff, pend, adm, inv, c1, c2, gc, gs);
+        }
     }
     // ---- epilogue (last CTA out): control block, R, next downdate's Givens
     if (!grid_exit(&c->bar, &c->bar_exit)) return;
@@ -342,7 +377,7 @@ static int mcb(int M) { return M <= 1 ? 1 : M <= 2 ? 2 : M <= 4 ? 4 : M <= 8 ? 8
 #define IG_FUSED_DISPATCH(KERNEL, ARGS, VEC_IN, NSM, STREAM)                                        \
     do {                                                                                            \
         const int mc = mcb((ARGS).M);                                                               \
-        const bool v2 = ((VEC_IN) == 2) && mc <= 8;                                                 \
+        const bool v2 = ((VEC_IN) == 2) && mc <= 16;                                                \
         switch (mc) {                                                                               \
         case 1: return v2 ? coop_launch(KERNEL<1, 2>, ARGS, NSM, STREAM)                            \
                           : coop_launch(KERNEL<1, 1>, ARGS, NSM, STREAM);                           \
@@ -352,7 +387,8 @@ static int mcb(int M) { return M <= 1 ? 1 : M <= 2 ? 2 : M <= 4 ? 4 : M <= 8 ? 8
                           : coop_launch(KERNEL<4, 1>, ARGS, NSM, STREAM);                           \
         case 8: return v2 ? coop_launch(KERNEL<8, 2>, ARGS, NSM, STREAM)                            \
                           : coop_launch(KERNEL<8, 1>, ARGS, NSM, STREAM);                           \
-        case 16: return coop_launch(KERNEL<16, 1>, ARGS, NSM, STREAM);                              \
+        case 16: return v2 ? coop_launch(KERNEL<16, 2>, ARGS, NSM, STREAM)                          \
+                           : coop_launch(KERNEL<16, 1>, ARGS, NSM, STREAM);                         \
         default: return coop_launch(KERNEL<32, 1>, ARGS, NSM, STREAM);                              \
         }                                                                                           \
     } while (0)

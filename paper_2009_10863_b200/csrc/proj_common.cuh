@@ -91,21 +91,22 @@ __device__ __forceinline__ void final_reduce(int nc, bool norm, const double *bl
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     constexpr int NW = THREADS / 32;
     constexpr int JS = (MC + 1 + NW - 1) / NW;
+    constexpr int CH = JS <= 2 ? 8 : 4;  // blocks per lane per round trip (register budget)
     const int nb = gridDim.x;
-    double s[JS][8];
+    double s[JS][CH];
 #pragma unroll
     for (int j = 0; j < JS; ++j)
 #pragma unroll
-        for (int u = 0; u < 8; ++u) s[j][u] = 0.0;
-    for (int base = lane; base < nb; base += 8 * 32) {
-        double t[JS][8];
+        for (int u = 0; u < CH; ++u) s[j][u] = 0.0;
+    for (int base = lane; base < nb; base += CH * 32) {
+        double t[JS][CH];
 #pragma unroll
         for (int j = 0; j < JS; ++j) {
             const int q = w + j * NW;  // compact slot index: q < MC -> coefficient q, q == MC -> norm
             const bool act = (q < MC) ? (q < nc) : (q == MC && norm);
             const int k = (q < MC) ? q : NORM;
 #pragma unroll
-            for (int u = 0; u < 8; ++u) {
+            for (int u = 0; u < CH; ++u) {
                 const int bb = base + u * 32;
                 t[j][u] = (act && bb < nb) ? __ldcg(blk + k * MAXB + bb) : 0.0;
             }
@@ -113,14 +114,15 @@ __device__ __forceinline__ void final_reduce(int nc, bool norm, const double *bl
 #pragma unroll
         for (int j = 0; j < JS; ++j)
 #pragma unroll
-            for (int u = 0; u < 8; ++u) s[j][u] += t[j][u];
+            for (int u = 0; u < CH; ++u) s[j][u] += t[j][u];
     }
 #pragma unroll
     for (int j = 0; j < JS; ++j) {
         const int q = w + j * NW;
         const bool act = (q < MC) ? (q < nc) : (q == MC && norm);
         if (!act) continue;  // warp-uniform
-        double t = ((s[j][0] + s[j][1]) + (s[j][2] + s[j][3])) + ((s[j][4] + s[j][5]) + (s[j][6] + s[j][7]));
+        double t = (s[j][0] + s[j][1]) + (s[j][2] + s[j][3]);
+        if (CH == 8) t += (s[j][CH > 4 ? 4 : 0] + s[j][CH > 5 ? 5 : 0]) + (s[j][CH > 6 ? 6 : 0] + s[j][CH > 7 ? 7 : 0]);
         t = warp_sum(t);
         if (lane == 0) out[(q < MC) ? q : NORM] = t;
     }
@@ -311,9 +313,9 @@ __device__ __forceinline__ void u3_elem(const ProjArgs &a, int64_t i, int deff, 
 
 // U-way unrolled variants (U strided elements per trip, all loads of the trip first): more bytes
 // in flight per thread for the passes that stream only d+1 vectors.
-template <int MC, int U, class V>
+template <int MC, int U, class V, class CP>
 __device__ __forceinline__ void u1_trip(const ProjArgs &a, int64_t i0, int64_t stride, int64_t nv, bool pend,
-                                        int deff, const double *gc, const double *gs, double (&v)[MC + 1]) {
+                                        int deff, CP gc, CP gs, double (&v)[MC + 1]) {
     const int nload = pend ? a.M : deff;
     V col[U][MC], ax[U];
 #pragma unroll
@@ -372,6 +374,10 @@ __device__ __forceinline__ void u2_trip(const ProjArgs &a, int64_t i0, int64_t s
 // Unroll of the fused kernels' d+1-stream passes (registers are sized by the X~ pass anyway).
 template <int MC> struct FusedUnroll {
     static constexpr int U = MC <= 4 ? 4 : (MC <= 8 ? 2 : 1);
+    static constexpr int U3 = MC <= 2 ? 4 : (MC <= 4 ? 2 : 1);  // X~ pass (2d+2 streams)
+    // For MC >= 16 the per-column coefficients (c1, c2, Givens c/s) are read from shared memory
+    // at each use instead of living in 4*MC registers, which the column loads need.
+    static constexpr bool SMEM_COEF = MC >= 16;
 };
 
 // One warp: Givens parameters of the next downdate from R (AMB-2 reading of P:279-290):

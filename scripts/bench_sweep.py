@@ -94,10 +94,11 @@ def main():
             for k in range(M + 1):
                 estep(k)
             te = time_steps(estep, a.steps)
+            nnz = sum(1 for w in he.weights() if w != 0.0)
             he.close()
             del he, X, AX, x0
             torch.cuda.empty_cache()
-            bq, be = (8 * M + 4) * vb, (M + 1) * vb
+            bq, be = (8 * M + 4) * vb, (nnz + 1) * vb
             ws_q = (2 * M + 3) * vb
             r = {"N": N, "M": M, "qr_us": tq, "qr_gbs": bq / (tq * 1e-6) / 1e9, "qr_frac": bq / (tq * 1e-6) / 1e9 / P,
                  "extrap_p": p, "extrap_us": te, "extrap_gbs": be / (te * 1e-6) / 1e9,

@@ -303,3 +303,44 @@ def test_c2_full_size_parity():
         x_prev = x
     hp.close()
     he.close()
+
+
+# ------------------------------------------------------------------ sparse extrapolation (NEXT row f2)
+@pytest.mark.parametrize("m,M", [(2, 8), (3, 8), (3, 16), (2, 12), (5, 30), (0, 4), (3, 4)])
+def test_sparse_weights_match_exact_cpqr(m, M):
+    from oracle import sparse_weights
+    from paper_2009_10863_b200 import InitialGuess
+
+    ig = InitialGuess(10, "extrap_sparse", M, m)
+    for f in range(1, M + 1):
+        w_o = sparse_weights(min(m, f - 1), f)
+        w_g = np.array(ig.weights(f))
+        assert np.array_equal(w_g != 0.0, w_o != 0.0), (f, w_g, w_o)  # same selected history
+        assert np.max(np.abs(w_g - w_o)) <= 1e-14 * max(1.0, np.abs(w_o).sum()), f
+    ig.close()
+
+
+@pytest.mark.parametrize("m,M", [(2, 8), (3, 16)])
+def test_sparse_open_loop_and_bytes(m, M):
+    from oracle import ExtrapSparse
+    from paper_2009_10863_b200 import InitialGuess
+
+    g = Grid(30, 2)
+    seq = _seq(g, M + 6)
+    ora = ExtrapSparse(g.N, M, m)
+    ig = InitialGuess(g.N, "extrap_sparse", M, m)
+    for n, (b, x, Ax) in enumerate(seq):
+        x0 = ig.next_slot()
+        if n == 0:
+            x0.zero_()
+        ig.form_guess(None, x0)
+        assert _rel(x0.cpu().numpy(), ora.form_guess(b, np.zeros(g.N))) <= TOL, n
+        if n >= M:  # steady: (m+2) values per element (Table 1) with the zero-copy push
+            fb, ub = ig.bytes()
+            assert fb == (m + 2) * 8 * g.N and ub == 0
+        ora.update(x)
+        x0.copy_(torch.from_numpy(x))
+        ig.update(x0)
+        if n >= M:
+            assert ig.bytes()[1] == 0
+    ig.close()
