@@ -3,7 +3,7 @@
 
 For each (N, M): QR(M) form+update and EXTRAP(floor(sqrt M), M) form+update (zero-copy push)
 timed with CUDA events over K steps after history fill; effective GB/s from the algorithmic
-bytes (QR (8M+4)*8N, EXTRAP (M+1)*8N), fraction of the measured copy roofline.  Inputs are
+bytes (QR (8M+4)*8N, EXTRAP (nnz(beta)+1)*8N), fraction of the measured copy roofline.  Inputs are
 random per-step vectors from a pool of M+2 (a vector re-enters only after it left the window, so
 every projection update is admitted and the full update path is timed).  Points whose per-step
 working set fits in L2 are labelled (L2-resident, not an HBM measurement).
