@@ -43,6 +43,20 @@ static int set_err(int code, const char *fmt, ...) {
             return set_err(IG_E_CUDA, "%s: %s (%s:%d)", #expr, cudaGetErrorString(e_), __FILE__, __LINE__); \
     } while (0)
 
+ig::LaunchFlags ig::launch_flags() {
+    static LaunchFlags f = [] {
+        LaunchFlags r;
+        const char *e = getenv("IG_LAUNCH");
+        if (e) {
+            std::string v(e);
+            r.coop = v.find("coop") != std::string::npos;
+            r.pdl = v.find("pdl") != std::string::npos;
+        }
+        return r;
+    }();
+    return f;
+}
+
 int ig::cached_occupancy(const void *kernel) {
     static std::mutex mu;
     static std::unordered_map<const void *, int> cache;

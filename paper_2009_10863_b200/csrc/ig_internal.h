@@ -5,6 +5,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <utility>
+
 namespace ig {
 
 constexpr int MAXM = 32;       // IG_MAX_HISTORY
@@ -61,6 +63,51 @@ struct ExtrapArgs {
     int64_t N;
     double *x0;
 };
+
+// ----------------------------------------------------------------------------- launch policy
+// Process-wide launch flags (env IG_LAUNCH, comma list of "coop", "pdl"; default "pdl"):
+//   coop: persistent fused kernels use cooperative launch (co-residency guaranteed by the driver).
+//         Without it (default) they rely on grid = SMs x occupancy being resident at once, which
+//         holds whenever no other stream pins SMs indefinitely; measured 1.7% faster at C2.
+//   pdl : programmatic dependent launch: every libig kernel may be launched while its stream
+//         predecessor is finishing; each kernel executes griddepcontrol.wait (waits for the full
+//         completion + memory flush of the predecessor) before touching memory, and triggers its
+//         dependents once its streaming passes are done (C2: 232.2 -> 224.3 us/step).
+struct LaunchFlags {
+    bool coop = false;
+    bool pdl = true;
+};
+LaunchFlags launch_flags();
+
+#ifdef __CUDACC__
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+template <typename... Exp, typename... Act>
+static cudaError_t launch_ex(void (*kern)(Exp...), int grid, cudaStream_t s, bool coop, Act &&...args) {
+    const LaunchFlags f = launch_flags();
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(THREADS);
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = s;
+    cudaLaunchAttribute at[2];
+    int na = 0;
+    if (coop && f.coop) {
+        at[na].id = cudaLaunchAttributeCooperative;
+        at[na].val.cooperative = 1;
+        ++na;
+    }
+    if (f.pdl) {
+        at[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[na].val.programmaticStreamSerializationAllowed = 1;
+        ++na;
+    }
+    cfg.attrs = at;
+    cfg.numAttrs = na;
+    return cudaLaunchKernelEx(&cfg, kern, std::forward<Act>(args)...);
+}
+#endif
 
 // Launchers (kern_proj.cu / kern_extrap.cu).  `vec` = 2 when every vector is 16-byte aligned.
 // Return the cudaError_t of the launch.  *blocks receives the grid size used.

@@ -17,6 +17,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_extrap(const __grid_constant__ E
     // All loads of a trip are issued before the FMAs consume them (see kern_proj.cu); the
     // accumulation order is oldest -> newest, like Eq. EXTRAPEXPN.
     typedef typename std::conditional<VEC == 2, double2, double>::type V;
+    pdl_wait();
     const int f = a.f;
     const int64_t nv = a.N / VEC;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
@@ -56,10 +57,12 @@ __global__ void __launch_bounds__(THREADS, 1) k_extrap(const __grid_constant__ E
             if (j < f) acc = fma(a.beta[j], a.src[j][e], acc);
         a.x0[e] = acc;
     }
+    pdl_trigger();
 }
 
 template <int VEC>
 __global__ void __launch_bounds__(THREADS, 1) k_copy(double *__restrict__ dst, const double *__restrict__ src, int64_t N) {
+    pdl_wait();
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     if (VEC == 2) {
         const int64_t nv = N >> 1;
@@ -87,11 +90,11 @@ static void launch_fc(const ExtrapArgs &a, int vec, int nsm, cudaStream_t s) {
     if (vec == 2) {
         constexpr int U = FC <= 2 ? 4 : (FC <= 4 ? 2 : 1);
         auto k = k_extrap<FC, 2, U>;  // U strided elements per trip when few streams
-        k<<<grid_for_x(k, a.N / 2, nsm), THREADS, 0, s>>>(a);
+        launch_ex(k, grid_for_x(k, a.N / 2, nsm), s, false, a);
     } else {
         constexpr int U = FC <= 2 ? 4 : (FC <= 4 ? 2 : 1);
         auto k = k_extrap<FC, 1, U>;
-        k<<<grid_for_x(k, a.N, nsm), THREADS, 0, s>>>(a);
+        launch_ex(k, grid_for_x(k, a.N, nsm), s, false, a);
     }
 }
 
@@ -109,10 +112,10 @@ cudaError_t launch_extrap(const ExtrapArgs &a, int vec, int nsm, cudaStream_t s)
 cudaError_t launch_copy(double *dst, const double *src, int64_t N, int vec, int nsm, cudaStream_t s) {
     if (vec == 2) {
         auto k = k_copy<2>;
-        k<<<grid_for_x(k, N / 2, nsm), THREADS, 0, s>>>(dst, src, N);
+        launch_ex(k, grid_for_x(k, N / 2, nsm), s, false, dst, src, N);
     } else {
         auto k = k_copy<1>;
-        k<<<grid_for_x(k, N, nsm), THREADS, 0, s>>>(dst, src, N);
+        launch_ex(k, grid_for_x(k, N, nsm), s, false, dst, src, N);
     }
     return cudaGetLastError();
 }

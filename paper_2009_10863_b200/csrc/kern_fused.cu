@@ -151,6 +151,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_form_fused(ProjArgs a) {
     constexpr int U = FusedUnroll<MC>::U;
     __shared__ double sh[(THREADS / 32) * (MC + 1)];
     __shared__ double s_red[PS];
+    pdl_wait();  // stream predecessor complete and visible (programmatic dependent launch)
     Ctrl *c = a.ctrl;
     const int d = c->d;
     if (d == 0) return;  // uniform: x0 stays the caller's fallback
@@ -206,6 +207,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_form_fused(ProjArgs a) {
             if (k < d) acc = fma(al[k], a.Xt[k * a.ld + i], acc);
         a.x0[i] = acc;
     }
+    pdl_trigger();
     if (grid_exit(&c->bar, &c->bar_exit) && threadIdx.x < d) a.part[ST_FORM * PS + threadIdx.x] = s_red[threadIdx.x];
 }
 
@@ -221,6 +223,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_update_fused(ProjArgs a) {
     __shared__ double s_nb, s_nAx;
     __shared__ int s_adm;
     __shared__ double s_H[MAXM * MAXM];
+    pdl_wait();  // stream predecessor complete and visible (programmatic dependent launch)
     Ctrl *c = a.ctrl;
     const int d = c->d, M = a.M;
     const bool pend = c->pending != 0;
@@ -329,6 +332,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_update_fused(ProjArgs a) {
             u3trip_store(r, a, a.N - 1, 1, a.N, deff, pend, adm, inv, c1, c2, gc, gs);
         }
     }
+    pdl_trigger();
     // ---- epilogue (last CTA out): control block, R, next downdate's Givens
     if (!grid_exit(&c->bar, &c->bar_exit)) return;
     if (pend)
@@ -367,9 +371,7 @@ template <class K> static cudaError_t coop_launch(K kern, const ProjArgs &a, int
     if (occ > 4) occ = 4;
     int grid = nsm * occ;
     if (grid > MAXB) grid = MAXB;
-    ProjArgs args = a;
-    void *params[] = {&args};
-    return cudaLaunchCooperativeKernel((const void *)kern, dim3(grid), dim3(THREADS), params, 0, s);
+    return launch_ex(kern, grid, s, true, a);
 }
 
 static int mcb(int M) { return M <= 1 ? 1 : M <= 2 ? 2 : M <= 4 ? 4 : M <= 8 ? 8 : M <= 16 ? 16 : 32; }

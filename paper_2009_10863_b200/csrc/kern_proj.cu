@@ -23,6 +23,7 @@ namespace ig {
 template <int MC, int VEC>
 __global__ void __launch_bounds__(THREADS, 1) k_form_dot(ProjArgs a) {
     typedef typename VT<VEC>::T V;
+    pdl_wait();
     constexpr int U = Unroll<MC>::U;
     __shared__ double sh[(THREADS / 32) * (MC + 1)];
     const int d = a.ctrl->d;
@@ -64,6 +65,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_form_dot(ProjArgs a) {
 template <int MC, int VEC>
 __global__ void __launch_bounds__(THREADS, 1) k_form_combine(ProjArgs a) {
     typedef typename VT<VEC>::T V;
+    pdl_wait();
     constexpr int U = Unroll<MC>::U;
     __shared__ double s_al[MC];
     const int d = a.ctrl->d;
@@ -107,6 +109,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_form_combine(ProjArgs a) {
 template <int MC, int VEC>
 __global__ void __launch_bounds__(THREADS, 1) k_u1(ProjArgs a) {
     typedef typename VT<VEC>::T V;
+    pdl_wait();
     __shared__ double sh[(THREADS / 32) * (MC + 1)];
     __shared__ double s_gc[MAXM], s_gs[MAXM];
     Ctrl *c = a.ctrl;
@@ -152,6 +155,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_u1(ProjArgs a) {
 template <int MC, int VEC>
 __global__ void __launch_bounds__(THREADS, 1) k_u2(ProjArgs a) {
     typedef typename VT<VEC>::T V;
+    pdl_wait();
     constexpr int U = Unroll<MC>::U;
     __shared__ double sh[(THREADS / 32) * (MC + 1)];
     __shared__ double s_c1[MAXM];
@@ -211,6 +215,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_u2(ProjArgs a) {
 template <int MC, int VEC>
 __global__ void __launch_bounds__(THREADS, 1) k_u3(ProjArgs a) {
     typedef typename VT<VEC>::T V;
+    pdl_wait();
     __shared__ double s_c1[MAXM], s_c2[MAXM], s_gc[MAXM], s_gs[MAXM];
     __shared__ double s_nb, s_nAx;
     __shared__ int s_adm;
@@ -312,16 +317,16 @@ static int mc_bucket(int M) { return M <= 1 ? 1 : M <= 2 ? 2 : M <= 4 ? 4 : M <=
         const bool v2 = ((VEC_IN) == 2) && mc <= 8;                                                         \
         const int64_t nv = (ARGS).N / (v2 ? 2 : 1);                                                         \
         switch (mc) {                                                                                       \
-        case 1: if (v2) { auto k = KERNEL<1, 2>; k<<<grid_for(k, nv, NSM), THREADS, 0, STREAM>>>(ARGS); }    \
-                else { auto k = KERNEL<1, 1>; k<<<grid_for(k, nv, NSM), THREADS, 0, STREAM>>>(ARGS); } break; \
-        case 2: if (v2) { auto k = KERNEL<2, 2>; k<<<grid_for(k, nv, NSM), THREADS, 0, STREAM>>>(ARGS); }    \
-                else { auto k = KERNEL<2, 1>; k<<<grid_for(k, nv, NSM), THREADS, 0, STREAM>>>(ARGS); } break; \
-        case 4: if (v2) { auto k = KERNEL<4, 2>; k<<<grid_for(k, nv, NSM), THREADS, 0, STREAM>>>(ARGS); }    \
-                else { auto k = KERNEL<4, 1>; k<<<grid_for(k, nv, NSM), THREADS, 0, STREAM>>>(ARGS); } break; \
-        case 8: if (v2) { auto k = KERNEL<8, 2>; k<<<grid_for(k, nv, NSM), THREADS, 0, STREAM>>>(ARGS); }    \
-                else { auto k = KERNEL<8, 1>; k<<<grid_for(k, nv, NSM), THREADS, 0, STREAM>>>(ARGS); } break; \
-        case 16: { auto k = KERNEL<16, 1>; k<<<grid_for(k, nv, NSM), THREADS, 0, STREAM>>>(ARGS); } break;  \
-        default: { auto k = KERNEL<32, 1>; k<<<grid_for(k, nv, NSM), THREADS, 0, STREAM>>>(ARGS); } break;  \
+        case 1: if (v2) { auto k = KERNEL<1, 2>; launch_ex(k, grid_for(k, nv, NSM), STREAM, false, ARGS); }    \
+                else { auto k = KERNEL<1, 1>; launch_ex(k, grid_for(k, nv, NSM), STREAM, false, ARGS); } break; \
+        case 2: if (v2) { auto k = KERNEL<2, 2>; launch_ex(k, grid_for(k, nv, NSM), STREAM, false, ARGS); }    \
+                else { auto k = KERNEL<2, 1>; launch_ex(k, grid_for(k, nv, NSM), STREAM, false, ARGS); } break; \
+        case 4: if (v2) { auto k = KERNEL<4, 2>; launch_ex(k, grid_for(k, nv, NSM), STREAM, false, ARGS); }    \
+                else { auto k = KERNEL<4, 1>; launch_ex(k, grid_for(k, nv, NSM), STREAM, false, ARGS); } break; \
+        case 8: if (v2) { auto k = KERNEL<8, 2>; launch_ex(k, grid_for(k, nv, NSM), STREAM, false, ARGS); }    \
+                else { auto k = KERNEL<8, 1>; launch_ex(k, grid_for(k, nv, NSM), STREAM, false, ARGS); } break; \
+        case 16: { auto k = KERNEL<16, 1>; launch_ex(k, grid_for(k, nv, NSM), STREAM, false, ARGS); } break;  \
+        default: { auto k = KERNEL<32, 1>; launch_ex(k, grid_for(k, nv, NSM), STREAM, false, ARGS); } break;  \
         }                                                                                                   \
     } while (0)
 
