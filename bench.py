@@ -356,7 +356,8 @@ def run_ours(args, world, rank, local):
     torch.cuda.synchronize()
     te = max_over_ranks(time.perf_counter() - t0, world)
     e2e = {"value": world * step_bytes * KE / te / 1e9, "unit": "GB/s", "ms_per_step": te / KE * 1e3,
-           "h2d_bytes_per_step": 5 * 8 * N, "d2h_bytes_per_step": 2 * 8 * N, "steps": KE,
+           "h2d_bytes_per_step": 4 * 8 * N, "d2h_bytes_per_step": 2 * 8 * N, "steps": KE,
+           "h2d_vectors": "QR: b, x, Ax (the fallback x0 is not uploaded once d > 0); EXTRAP: x",
            "api": "ig_form_guess_host/ig_update_host (pinned host buffers)"}
 
     # ---- CPU oracle baseline (rank 0, N=1 only)

@@ -145,6 +145,7 @@ struct ig_ctx {
     int last_form_f = 0;
     // host staging (end-to-end path)
     double *stage[4] = {nullptr, nullptr, nullptr, nullptr};
+    int known_d = 0;  // projection d as of the last synchronising host-buffer call (-1: unknown)
     int64_t launches = 0;
     // per-kernel CUDA-event timing (ig_profile)
     bool profiling = false;
@@ -379,6 +380,7 @@ int ig_reset(ig_t h) {
     DevGuard g(h->dev);
     if (is_proj(h->method)) CUDA_OK(cudaMemsetAsync(h->ctrl, 0, sizeof(Ctrl), h->stream));
     h->head = h->fill = 0;
+    h->known_d = 0;
     return IG_OK;
 }
 
@@ -506,7 +508,22 @@ int ig_form_guess_host(ig_t h, const double *b, double *x0) {
     if (is_proj(h->method)) {
         if (!b) return set_err(IG_E_ARG, "b is NULL");
         CUDA_OK(cudaMemcpyAsync(h->stage[0], b, nb, cudaMemcpyHostToDevice, h->stream));
-        CUDA_OK(cudaMemcpyAsync(h->stage[1], x0, nb, cudaMemcpyHostToDevice, h->stream));
+        // the fallback x0 is only read when d == 0: skip its upload otherwise
+        if (h->known_d != 0) {
+            int d = 0;
+            rc = ig_history_dim(h, &d);
+            if (rc) return rc;
+            h->known_d = d;
+        }
+        if (h->known_d == 0) {
+            CUDA_OK(cudaMemcpyAsync(h->stage[1], x0, nb, cudaMemcpyHostToDevice, h->stream));
+        } else {
+            rc = ig_form_guess(h, h->stage[0], h->stage[1]);
+            if (rc) return rc;
+            CUDA_OK(cudaMemcpyAsync(x0, h->stage[1], nb, cudaMemcpyDeviceToHost, h->stream));
+            CUDA_OK(cudaStreamSynchronize(h->stream));
+            return IG_OK;
+        }
         rc = ig_form_guess(h, h->stage[0], h->stage[1]);
         if (rc) return rc;
     } else {
@@ -531,6 +548,7 @@ int ig_update_host(ig_t h, const double *x, const double *Ax) {
         CUDA_OK(cudaMemcpyAsync(h->stage[3], Ax, nb, cudaMemcpyHostToDevice, h->stream));
         rc = ig_update(h, h->stage[2], h->stage[3]);
         if (rc) return rc;
+        h->known_d = -1;  // re-read (4 bytes) by the next ig_form_guess_host
     } else {
         double *slot = next_slot_ptr(h);  // copy straight into the ring slot: zero-copy push
         CUDA_OK(cudaMemcpyAsync(slot, x, nb, cudaMemcpyHostToDevice, h->stream));
