@@ -92,7 +92,11 @@ int build_ls_weights(int m, int M, double *beta) {
         y[j] = s / V[(size_t)j * cols + j];
     }
     apply_q(V, M, cols, tau, y.data());  // beta = Q [w; 0]
-    for (int i = 0; i < M; ++i) beta[i] = y[i];
+    // Weights that are zero in exact arithmetic (e.g. beta_4 of EXTRAP(3,8) = 0) come out at the
+    // rounding level; snap them so the kernel does not stream that solution at all.
+    double l1 = 0.0;
+    for (int i = 0; i < M; ++i) l1 += std::fabs(y[i]);
+    for (int i = 0; i < M; ++i) beta[i] = (std::fabs(y[i]) <= 4e-16 * M * l1) ? 0.0 : y[i];
     return 0;
 }
 
