@@ -81,10 +81,20 @@ __device__ __forceinline__ void u2trip_compute(const U2Trip<MC, U, V> &r, CP c1,
     }
 }
 
+// For MC >= 32 (SPLIT) a trip holds only Ax, x and the B~ columns; the X~ columns are loaded
+// (all at once) after the B~ part is finished, so the two 32-column register sets are never live
+// together and the pass can use 16-byte loads (VEC = 2) within the register file.
 template <int MC, int U, class V> struct U3Trip {  // update pass 3: U strided elements
+    static constexpr bool SPLIT = MC >= 32;
     V ax[U], xv[U];
-    V bc[U][MC], xc[U][MC];
+    V bc[U][MC];
+    V xc[U][SPLIT ? 1 : MC];
 };
+template <int MC, class V>
+__device__ __forceinline__ void u3_load_x(V (&xc)[MC], const ProjArgs &a, int64_t i, bool ok, int nX) {
+#pragma unroll
+    for (int k = 0; k < MC; ++k) xc[k] = (ok && k < nX) ? ldrw<V>(a.Xt + k * a.ld, i) : vzero(V());
+}
 // Loads assume the pair is admitted (the common case); if it is not, the prefetched B~/Ax/x
 // values of that one trip are simply unused.
 template <int MC, int U, class V>
@@ -100,8 +110,30 @@ __device__ __forceinline__ void u3trip_load(U3Trip<MC, U, V> &r, const ProjArgs 
         r.xv[u] = (ok && adm) ? ldro<V>(a.x, i) : vzero(V());
 #pragma unroll
         for (int k = 0; k < MC; ++k) r.bc[u][k] = (ok && k < nB) ? ldrw<V>(a.Bt + k * a.ld, i) : vzero(V());
+        if constexpr (!U3Trip<MC, U, V>::SPLIT) u3_load_x<MC, V>(r.xc[u], a, i, ok, nX);
+    }
+}
+template <int MC, class V, class CP>
+__device__ __forceinline__ void u3_x_part(const V (&xc)[MC], const ProjArgs &a, int64_t i, bool rotX, V &xt, V &t2,
+                                          CP c1, CP c2, CP gc, CP gs) {
+    if (rotX) {
+        V t = xc[0];
 #pragma unroll
-        for (int k = 0; k < MC; ++k) r.xc[u][k] = (ok && k < nX) ? ldrw<V>(a.Xt + k * a.ld, i) : vzero(V());
+        for (int k = 0; k < MC - 1; ++k) {
+            if (k < a.M - 1) {
+                V nk;
+                vrot(gc[k], gs[k], t, xc[k + 1], nk);
+                stv<V>(a.Xt + k * a.ld, i, nk);
+                xt = vaxpy(-c1[k], nk, xt);
+                t2 = vaxpy(c2[k], nk, t2);
+            }
+        }
+    } else {
+#pragma unroll
+        for (int k = 0; k < MC; ++k) {
+            xt = vaxpy(-c1[k], xc[k], xt);
+            t2 = vaxpy(c2[k], xc[k], t2);
+        }
     }
 }
 template <int MC, int U, class V, class CP>
@@ -118,30 +150,16 @@ __device__ __forceinline__ void u3trip_store(const U3Trip<MC, U, V> &r, const Pr
         for (int k = 0; k < MC; ++k) b1 = vaxpy(-c1[k], r.bc[u][k], b1);
 #pragma unroll
         for (int k = 0; k < MC; ++k) s2 = vaxpy(c2[k], r.bc[u][k], s2);
+        if (adm) stv<V>(a.Bt + deff * a.ld, i, vscale(inv, vaxpy(-1.0, s2, b1)));
         V xt = r.xv[u], t2 = vzero(V());
-        if (rotX) {
-            V t = r.xc[u][0];
-#pragma unroll
-            for (int k = 0; k < MC - 1; ++k) {
-                if (k < a.M - 1) {
-                    V nk;
-                    vrot(gc[k], gs[k], t, r.xc[u][k + 1], nk);
-                    stv<V>(a.Xt + k * a.ld, i, nk);
-                    xt = vaxpy(-c1[k], nk, xt);
-                    t2 = vaxpy(c2[k], nk, t2);
-                }
-            }
+        if constexpr (U3Trip<MC, U, V>::SPLIT) {
+            V xc[MC];
+            u3_load_x<MC, V>(xc, a, i, true, rotX ? a.M : (adm ? deff : 0));
+            u3_x_part<MC, V>(xc, a, i, rotX, xt, t2, c1, c2, gc, gs);
         } else {
-#pragma unroll
-            for (int k = 0; k < MC; ++k) {
-                xt = vaxpy(-c1[k], r.xc[u][k], xt);
-                t2 = vaxpy(c2[k], r.xc[u][k], t2);
-            }
+            u3_x_part<MC, V>(r.xc[u], a, i, rotX, xt, t2, c1, c2, gc, gs);
         }
-        if (adm) {
-            stv<V>(a.Bt + deff * a.ld, i, vscale(inv, vaxpy(-1.0, s2, b1)));
-            stv<V>(a.Xt + deff * a.ld, i, vscale(inv, vaxpy(-1.0, t2, xt)));
-        }
+        if (adm) stv<V>(a.Xt + deff * a.ld, i, vscale(inv, vaxpy(-1.0, t2, xt)));
     }
 }
 
@@ -379,7 +397,7 @@ static int mcb(int M) { return M <= 1 ? 1 : M <= 2 ? 2 : M <= 4 ? 4 : M <= 8 ? 8
 #define IG_FUSED_DISPATCH(KERNEL, ARGS, VEC_IN, NSM, STREAM)                                        \
     do {                                                                                            \
         const int mc = mcb((ARGS).M);                                                               \
-        const bool v2 = ((VEC_IN) == 2) && mc <= 16;                                                \
+        const bool v2 = ((VEC_IN) == 2);                                                            \
         switch (mc) {                                                                               \
         case 1: return v2 ? coop_launch(KERNEL<1, 2>, ARGS, NSM, STREAM)                            \
                           : coop_launch(KERNEL<1, 1>, ARGS, NSM, STREAM);                           \
@@ -391,7 +409,8 @@ static int mcb(int M) { return M <= 1 ? 1 : M <= 2 ? 2 : M <= 4 ? 4 : M <= 8 ? 8
                           : coop_launch(KERNEL<8, 1>, ARGS, NSM, STREAM);                           \
         case 16: return v2 ? coop_launch(KERNEL<16, 2>, ARGS, NSM, STREAM)                          \
                            : coop_launch(KERNEL<16, 1>, ARGS, NSM, STREAM);                         \
-        default: return coop_launch(KERNEL<32, 1>, ARGS, NSM, STREAM);                              \
+        default: return v2 ? coop_launch(KERNEL<32, 2>, ARGS, NSM, STREAM)                          \
+                           : coop_launch(KERNEL<32, 1>, ARGS, NSM, STREAM);                         \
         }                                                                                           \
     } while (0)
 
