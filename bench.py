@@ -47,6 +47,8 @@ def parse():
     p.add_argument("--e2e-steps", type=int, default=20)
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-seconds", type=float, default=15.0, help="budget of the oracle cpu_baseline sample")
+    p.add_argument("--exchange", choices=["peer", "nccl"], default="peer",
+                   help="N>1 projection sums: in-kernel NVLink peer exchange (fused) or NCCL between kernels")
     return p.parse_args()
 
 
@@ -239,7 +241,7 @@ def run_ours(args, world, rank, local):
     import torch
 
     from paper_2009_10863_b200 import (InitialGuess, comm_from_process_group, ig_form_guess_host, ig_profile,
-                                       ig_profile_read, ig_total_launches, ig_update_host)
+                                       ig_profile_read, ig_total_launches, ig_update_host, peers_from_process_group)
     from workloads.gen import manufactured_step_slab
 
     n, M, p = args.n, args.m, args.degree
@@ -253,8 +255,10 @@ def run_ours(args, world, rank, local):
     pool = [manufactured_step_slab(n, n, rank, world, k, device=dev) for k in range(S)]
     torch.cuda.synchronize()
 
-    comm = comm_from_process_group() if world > 1 else None
+    comm = comm_from_process_group() if (world > 1 and args.exchange == "nccl") else None
     hp = InitialGuess(N, "proj_qr", M, comm=comm)
+    if world > 1 and args.exchange == "peer":
+        peers_from_process_group([hp.h])
     he = InitialGuess(N, "extrap_ls", M, p)
     x0p = torch.zeros(N, dtype=torch.float64, device=dev)
     x0e = torch.zeros(N, dtype=torch.float64, device=dev)
@@ -382,7 +386,8 @@ def run_ours(args, world, rank, local):
                           "extrap_nnz": nnz,
                           "l2": f"fresh inputs every step; per-step working set "
                                 f"{(2 * M + M + 5) * 8 * N / 1e9:.2f} GB > L2 126 MB",
-                          "parallelism": f"dof-shard{world}" if world > 1 else "single"},
+                          "parallelism": f"dof-shard{world}" if world > 1 else "single",
+                          "exchange": (args.exchange if world > 1 else "none")},
                "gpu_launches": launches, "roofline": roofline, "kernels": kernels,
                "clocks": sampler.summary(), "e2e": e2e, "cpu_baseline": cpu,
                "proj_state": {"d": st["d"], "rho_last": st["rho"]}, "host_enqueue_us_per_step": host_us}

@@ -139,6 +139,26 @@ void ig_comm_destroy(ig_comm_t c);
  * N is then the LOCAL slice length; ranks may have different N. */
 int ig_attach_comm(ig_t h, ig_comm_t c);
 
+/* In-kernel exchange over NVLink peer memory (fused compute + collective):
+ * each projection handle owns a small exchange window (ig_xwin_bytes(), < 40 KB); after every
+ * reduction pass the persistent kernel's CTA 0 stores the rank-local partial sums into EVERY
+ * rank's window and releases an epoch flag (system scope); every CTA acquires the G flags and
+ * sums the G contributions in rank order (bitwise-identical on all ranks).  No NCCL launch and
+ * no host involvement per step.  Collective setup, all ranks (one handle each):
+ *   ig_xwin_export(h, handle64)  -> CUDA IPC handle of this rank's window (64 bytes);
+ *   exchange the handles (e.g. torch.distributed all-gather), then
+ *   ig_attach_peers(h, nranks, rank, handles (nranks*64 bytes), NULL).
+ * Ranks inside ONE process on the same GPU (virtual ranks, used by the single-GPU tests) pass
+ * peer_ptrs[r] = ig_xwin_ptr(h_r) instead of IPC handles; such ranks must run on different
+ * streams with grids that fit together (ig_set_grid_limit).  nranks <= 8.  All ranks must issue
+ * the same sequence of ig_form_guess / ig_update / ig_reset calls. */
+size_t ig_xwin_bytes(void);
+int ig_xwin_export(ig_t h, void *ipc_handle_out);
+void *ig_xwin_ptr(ig_t h);
+int ig_attach_peers(ig_t h, int nranks, int rank, const void *ipc_handles, void *const *peer_ptrs);
+/* Cap the grid of the persistent kernels (0 = SMs x occupancy). */
+int ig_set_grid_limit(ig_t h, int max_blocks);
+
 /* ---------------------------------------------------------------- introspection (tests/bench) */
 
 /* Current history dimension d (projection) or fill (extrapolation).  Syncs. */

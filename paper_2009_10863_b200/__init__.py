@@ -37,4 +37,10 @@ from .ig import (  # noqa: F401
     ig_update_host,
     ig_weights,
     shard_range,
+    ig_set_grid_limit,
+    ig_xwin_export,
+    ig_xwin_ptr,
+    ig_attach_peers,
+    peers_from_process_group,
+    attach_virtual_ranks,
 )

@@ -52,6 +52,11 @@ _SIGS = {
     "ig_copy_history": (C.c_int, [_P, _P, _P, C.c_int64, _D]),
     "ig_total_launches": (C.c_int64, []),
     "ig_profile": (C.c_int, [_P, C.c_int]),
+    "ig_xwin_bytes": (C.c_size_t, []),
+    "ig_xwin_export": (C.c_int, [_P, _P]),
+    "ig_xwin_ptr": (_P, [_P]),
+    "ig_attach_peers": (C.c_int, [_P, C.c_int, C.c_int, _P, C.POINTER(_P)]),
+    "ig_set_grid_limit": (C.c_int, [_P, C.c_int]),
     "ig_profile_read": (C.c_int, [_P, C.c_int, _D, C.POINTER(C.c_int64)]),
 }
 

@@ -137,6 +137,11 @@ struct ig_ctx {
     int G = 1;
     bool fused = true;  // persistent fused kernels when G == 1 (ig_set_schedule)
     ig_comm_ctx *comm = nullptr;
+    int max_grid = 0;   // ig_set_grid_limit
+    // in-kernel peer exchange (ig_attach_peers)
+    XWin *xwin = nullptr;
+    Exchange xc = {};
+    std::vector<void *> ipc_opened;
     // extrapolation
     std::vector<std::vector<double>> table;  // table[f-1]: weights for f stored solutions
     std::vector<double *> slots;
@@ -237,8 +242,14 @@ ProjArgs proj_args(ig_t h) {
     a.part = h->part;
     a.gath = h->gath;
     a.G = h->G;
+    a.max_grid = h->max_grid;
+    a.xc = h->xc;
     return a;
 }
+
+// Fused persistent kernels are used on one rank and with the in-kernel peer exchange; a NCCL
+// communicator without peer windows uses one kernel per pass with NCCL between them.
+bool use_fused(ig_t h) { return h->fused && (h->G == 1 || h->xc.G > 1); }
 
 int exchange(ig_t h, int stage) {
     if (h->G <= 1) return IG_OK;
@@ -350,6 +361,8 @@ void ig_destroy(ig_t h) {
     if (h->gath != h->part) cudaFree(h->gath);
     cudaFree(h->part);
     for (auto &s : h->stage) cudaFree(s);
+    for (void *p : h->ipc_opened) cudaIpcCloseMemHandle(p);
+    cudaFree(h->xwin);
     prof_drain(h);
     for (auto e : h->ev_pool) cudaEventDestroy(e);
     delete h;
@@ -378,7 +391,13 @@ int ig_set_admit_tol(ig_t h, double eps) {
 int ig_reset(ig_t h) {
     if (!h) return set_err(IG_E_ARG, "NULL handle");
     DevGuard g(h->dev);
-    if (is_proj(h->method)) CUDA_OK(cudaMemsetAsync(h->ctrl, 0, sizeof(Ctrl), h->stream));
+    if (is_proj(h->method)) {
+        // everything but the peer-exchange epochs, which stay monotonic across resets (every
+        // rank resets at the same point of the call sequence)
+        CUDA_OK(cudaMemsetAsync(h->ctrl, 0, offsetof(Ctrl, xepoch), h->stream));
+        const size_t tail = offsetof(Ctrl, xepoch) + sizeof(((Ctrl *)0)->xepoch);
+        CUDA_OK(cudaMemsetAsync(reinterpret_cast<char *>(h->ctrl) + tail, 0, sizeof(Ctrl) - tail, h->stream));
+    }
     h->head = h->fill = 0;
     h->known_d = 0;
     return IG_OK;
@@ -394,7 +413,7 @@ int ig_form_guess(ig_t h, const double *b, double *x0) {
         a.b = b;
         a.x0 = x0;
         const int vec = (al16(b) && al16(x0)) ? 2 : 1;
-        if (h->G == 1 && h->fused) {
+        if (use_fused(h)) {
             Prof p(h, IG_K_FORM_FUSED);
             CUDA_OK(launch_form_fused(a, vec, h->nsm, h->stream));
             count(h, 1);
@@ -453,7 +472,7 @@ int ig_update(ig_t h, const double *x, const double *Ax) {
         a.x = x;
         a.Ax = Ax;
         const int vec = (al16(x) && al16(Ax)) ? 2 : 1;
-        if (h->G == 1 && h->fused) {
+        if (use_fused(h)) {
             Prof p(h, IG_K_UPDATE_FUSED);
             CUDA_OK(launch_update_fused(a, vec, h->nsm, h->stream));
             count(h, 1);
@@ -613,6 +632,73 @@ int ig_attach_comm(ig_t h, ig_comm_t c) {
     CUDA_OK(cudaMemset(gb, 0, sizeof(double) * PS * NSTAGE * c->nranks));
     h->gath = gb;
     h->G = c->nranks;
+    return IG_OK;
+}
+
+int ig_set_grid_limit(ig_t h, int max_blocks) {
+    if (!h || max_blocks < 0) return set_err(IG_E_ARG, "bad handle or grid limit");
+    h->max_grid = max_blocks;
+    return IG_OK;
+}
+
+static int ensure_xwin(ig_t h) {
+    if (!is_proj(h->method)) return set_err(IG_E_ARG, "peer exchange is for projection handles");
+    if (h->xwin) return IG_OK;
+    if (cudaMalloc(&h->xwin, sizeof(XWin)) != cudaSuccess) {
+        cudaGetLastError();
+        h->xwin = nullptr;
+        return set_err(IG_E_OOM, "exchange window allocation failed");
+    }
+    CUDA_OK(cudaMemset(h->xwin, 0, sizeof(XWin)));
+    return IG_OK;
+}
+
+size_t ig_xwin_bytes(void) { return sizeof(XWin); }
+
+int ig_xwin_export(ig_t h, void *ipc_handle_out) {
+    if (!h || !ipc_handle_out) return set_err(IG_E_ARG, "NULL argument");
+    DevGuard g(h->dev);
+    int rc = ensure_xwin(h);
+    if (rc) return rc;
+    cudaIpcMemHandle_t mh;
+    CUDA_OK(cudaIpcGetMemHandle(&mh, h->xwin));
+    static_assert(sizeof(mh) == 64, "CUDA IPC handle is 64 bytes");
+    memcpy(ipc_handle_out, &mh, 64);
+    return IG_OK;
+}
+
+void *ig_xwin_ptr(ig_t h) {
+    if (!h) return nullptr;
+    DevGuard g(h->dev);
+    if (ensure_xwin(h)) return nullptr;
+    return h->xwin;
+}
+
+int ig_attach_peers(ig_t h, int nranks, int rank, const void *ipc_handles, void *const *peer_ptrs) {
+    if (!h || nranks < 1 || nranks > MAXG || rank < 0 || rank >= nranks)
+        return set_err(IG_E_ARG, "bad peer arguments (1 <= nranks <= %d)", MAXG);
+    DevGuard g(h->dev);
+    int rc = ensure_xwin(h);
+    if (rc) return rc;
+    Exchange xc = {};
+    xc.G = nranks;
+    xc.rank = rank;
+    for (int r = 0; r < nranks; ++r) {
+        if (r == rank) {
+            xc.peer[r] = h->xwin;
+        } else if (peer_ptrs && peer_ptrs[r]) {
+            xc.peer[r] = static_cast<XWin *>(peer_ptrs[r]);  // same process (virtual ranks)
+        } else {
+            if (!ipc_handles) return set_err(IG_E_ARG, "rank %d: neither a pointer nor an IPC handle", r);
+            cudaIpcMemHandle_t mh;
+            memcpy(&mh, static_cast<const char *>(ipc_handles) + 64 * r, 64);
+            void *p = nullptr;
+            CUDA_OK(cudaIpcOpenMemHandle(&p, mh, cudaIpcMemLazyEnablePeerAccess));
+            h->ipc_opened.push_back(p);
+            xc.peer[r] = static_cast<XWin *>(p);
+        }
+    }
+    h->xc = nranks > 1 ? xc : Exchange{};
     return IG_OK;
 }
 

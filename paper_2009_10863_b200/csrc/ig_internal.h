@@ -16,6 +16,21 @@ constexpr int MAXB = 1024;     // max blocks of a reduction kernel (block-partia
 constexpr int THREADS = 256;   // threads per block of every streaming kernel
 
 enum Stage { ST_FORM = 0, ST_U1 = 1, ST_U2 = 2, ST_U3 = 3, NSTAGE = 4 };
+constexpr int MAXG = 8;        // ranks of an in-kernel peer-memory exchange (one NVLink node)
+
+// Exchange window of one rank, written by every rank over NVLink peer memory (or, for ranks in
+// one process, ordinary device memory): data[stage][epoch parity][sender][slot] and a monotonic
+// epoch flag per (stage, sender).  Parity double-buffering lets a fast rank publish epoch e+1
+// while a slow rank may still be reading epoch e.
+struct XWin {
+    double data[NSTAGE][2][MAXG][PS];
+    unsigned long long flag[NSTAGE][MAXG];
+};
+struct Exchange {
+    XWin *peer[MAXG];  // every rank's window, indexed by rank (peer[rank] == own window)
+    int G;             // ranks (0: no peer exchange)
+    int rank;
+};
 enum Method { M_PROJ_QR = 1, M_EXTRAP_LS = 2, M_PROJ_CLASSIC = 3, M_EXTRAP_SPARSE = 4 };
 
 // Device-resident state of one projection handle.  Every control decision (d, downdate,
@@ -30,6 +45,7 @@ struct Ctrl {
     int last_rot;   // the last update applied a downdate (bytes accounting)
     unsigned ticket[NSTAGE];
     unsigned bar, bar_exit;        // grid barrier / exit counters of the fused kernels
+    unsigned long long xepoch[NSTAGE];  // completed peer exchanges per stage (all ranks agree)
     double rho, nAx, nb;
     double gc[MAXM], gs[MAXM];      // Givens (c_i, s_i) of the pending downdate
     double R[MAXM * MAXM];          // R, column-major R(i,j) = R[i + j*MAXM]
@@ -53,6 +69,8 @@ struct ProjArgs {
     double *x0;            // form: guess (out)
     const double *x;       // update: solution
     const double *Ax;      // update: A x
+    int max_grid;          // cap on the persistent kernels' grid (0: SMs x occupancy)
+    Exchange xc;           // in-kernel peer exchange (xc.G > 1) for the fused kernels
 };
 
 struct ExtrapArgs {

@@ -173,6 +173,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_form_fused(ProjArgs a) {
     Ctrl *c = a.ctrl;
     const int d = c->d;
     if (d == 0) return;  // uniform: x0 stays the caller's fallback
+    const unsigned long long ep = c->xepoch[ST_FORM] + 1;
     const int64_t nv = a.N / VEC;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     const int64_t i_first = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -207,6 +208,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_form_fused(ProjArgs a) {
     block_partials_store<MC + 1>(v, d, false, a.blk, sh);
     grid_barrier(&c->bar, 1);
     reduce_all_blocks<MC>(d, false, a.blk, s_red);
+    if (a.xc.G > 1) peer_allreduce(a.xc, ST_FORM, d, false, s_red, ep);
     double al[MC];
 #pragma unroll
     for (int k = 0; k < MC; ++k) al[k] = (k < d) ? s_red[k] : 0.0;
@@ -226,7 +228,10 @@ __global__ void __launch_bounds__(THREADS, 1) k_form_fused(ProjArgs a) {
         a.x0[i] = acc;
     }
     pdl_trigger();
-    if (grid_exit(&c->bar, &c->bar_exit) && threadIdx.x < d) a.part[ST_FORM * PS + threadIdx.x] = s_red[threadIdx.x];
+    if (grid_exit(&c->bar, &c->bar_exit)) {
+        if (threadIdx.x < d) a.part[ST_FORM * PS + threadIdx.x] = s_red[threadIdx.x];
+        if (threadIdx.x == 0 && a.xc.G > 1) c->xepoch[ST_FORM] = ep;
+    }
 }
 
 template <int MC, int VEC>
@@ -247,6 +252,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_update_fused(ProjArgs a) {
     const bool pend = c->pending != 0;
     const bool restart = (a.method == M_PROJ_CLASSIC) && (d >= M);  // Alg. 1 restart
     const int deff = pend ? M - 1 : (restart ? 0 : d);
+    const unsigned long long ep1 = c->xepoch[ST_U1] + 1, ep2 = c->xepoch[ST_U2] + 1;
     if (threadIdx.x < MAXM) {
         const bool rot = pend && threadIdx.x < M - 1;
         s_gc[threadIdx.x] = rot ? c->gc[threadIdx.x] : 1.0;
@@ -285,6 +291,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_update_fused(ProjArgs a) {
     block_partials_store<MC + 1>(v, deff, true, a.blk, sh);
     grid_barrier(&c->bar, 1);
     reduce_all_blocks<MC>(deff, true, a.blk, s_r1);
+    if (a.xc.G > 1) peer_allreduce(a.xc, ST_U1, deff, true, s_r1, ep1);
     if (threadIdx.x < MAXM) s_c1[threadIdx.x] = (threadIdx.x < deff) ? s_r1[threadIdx.x] : 0.0;
     __syncthreads();
     if constexpr (!SMC) {
@@ -312,6 +319,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_update_fused(ProjArgs a) {
     if (deff > 0) block_partials_store<MC + 1>(v, deff, true, a.blk + BLK2, sh);
     grid_barrier(&c->bar, 2);
     if (deff > 0) reduce_all_blocks<MC>(deff, true, a.blk + BLK2, s_r2);
+    if (deff > 0 && a.xc.G > 1) peer_allreduce(a.xc, ST_U2, deff, true, s_r2, ep2);
     if (threadIdx.x == 0) {
         const double nAx2 = s_r1[NORM];
         double nb2;
@@ -376,6 +384,10 @@ __global__ void __launch_bounds__(THREADS, 1) k_update_fused(ProjArgs a) {
         c->rho = (s_nAx > 0.0) ? s_nb / s_nAx : 0.0;
         c->last_rot = pend ? 1 : 0;
         c->rotX = 0;
+        if (a.xc.G > 1) {
+            c->xepoch[ST_U1] = ep1;
+            if (deff > 0) c->xepoch[ST_U2] = ep2;
+        }
     }
     __syncthreads();
     if (a.method == M_PROJ_QR && dnew == M && threadIdx.x < 32) givens_plan(c, M, s_H);
@@ -388,6 +400,7 @@ template <class K> static cudaError_t coop_launch(K kern, const ProjArgs &a, int
     if (occ < 1) return cudaErrorInvalidConfiguration;
     if (occ > 4) occ = 4;
     int grid = nsm * occ;
+    if (a.max_grid > 0 && grid > a.max_grid) grid = a.max_grid;
     if (grid > MAXB) grid = MAXB;
     return launch_ex(kern, grid, s, true, a);
 }

@@ -200,6 +200,58 @@ __device__ __forceinline__ void reduce_all_blocks(int nc, bool norm, const doubl
     __syncthreads();
 }
 
+// ------------------------------------------------------------------ in-kernel peer exchange
+__device__ __forceinline__ void st_release_sys_u64(unsigned long long *p, unsigned long long v) {
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_acquire_sys_u64(const unsigned long long *p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ double ld_relaxed_sys_f64(const double *p) {
+    double v;
+    asm volatile("ld.relaxed.sys.global.f64 %0, [%1];" : "=d"(v) : "l"(p) : "memory");
+    return v;
+}
+
+// Cross-rank sum of one reduction pass inside the persistent kernel, over NVLink peer memory
+// (fused compute + collective, replacing the host-launched NCCL all-gather of the split path).
+// Every CTA holds the rank-local sums in shared `buf`; CTA 0 stores them into EVERY rank's window
+// (remote stores), fences at system scope and releases a per-(stage, sender) epoch flag; every CTA
+// acquires all G flags and sums the G contributions in RANK ORDER, so all ranks (and all CTAs)
+// get bitwise-identical results.  `buf` is overwritten with the global sums.
+__device__ __forceinline__ void peer_allreduce(const Exchange &xc, int stage, int nc, bool norm, double *buf,
+                                               unsigned long long epoch) {
+    const int par = (int)(epoch & 1ull);
+    const int G = xc.G, me = xc.rank;
+    if (blockIdx.x == 0) {
+        for (int idx = threadIdx.x; idx < G * PS; idx += blockDim.x) {
+            const int r = idx / PS, k = idx % PS;
+            const bool act = (k < MAXM) ? (k < nc) : norm;
+            if (act) xc.peer[r]->data[stage][par][me][k] = buf[k];
+        }
+        __threadfence_system();
+        __syncthreads();
+        if (threadIdx.x < G) st_release_sys_u64(&xc.peer[threadIdx.x]->flag[stage][me], epoch);
+    }
+    if (threadIdx.x == 0) {
+        const XWin *w = xc.peer[me];
+        for (int r = 0; r < G; ++r)
+            while (ld_acquire_sys_u64(&w->flag[stage][r]) < epoch) __nanosleep(32);
+    }
+    __syncthreads();
+    for (int k = threadIdx.x; k < PS; k += blockDim.x) {
+        const bool act = (k < MAXM) ? (k < nc) : norm;
+        if (!act) continue;
+        const XWin *w = xc.peer[me];
+        double s = ld_relaxed_sys_f64(&w->data[stage][par][0][k]);
+        for (int r = 1; r < G; ++r) s += ld_relaxed_sys_f64(&w->data[stage][par][r][k]);
+        buf[k] = s;
+    }
+    __syncthreads();
+}
+
 // Rank-ordered sum of the gathered partials of one stage.
 __device__ __forceinline__ double rank_sum(const double *g, int G, int k) {
     double s = g[k];

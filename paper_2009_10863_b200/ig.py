@@ -220,6 +220,53 @@ def comm_from_process_group(group=None):
     return ig_comm_create(world, rank, obj[0])
 
 
+def ig_set_grid_limit(h, max_blocks: int) -> None:
+    _check(lib().ig_set_grid_limit(h, int(max_blocks)), "ig_set_grid_limit")
+
+
+def ig_xwin_export(h) -> bytes:
+    buf = (C.c_char * 64)()
+    _check(lib().ig_xwin_export(h, buf), "ig_xwin_export")
+    return bytes(buf)
+
+
+def ig_xwin_ptr(h) -> int:
+    p = lib().ig_xwin_ptr(h)
+    if not p:
+        raise IGError(IG_E_ARG, "ig_xwin_ptr")
+    return p
+
+
+def ig_attach_peers(h, nranks: int, rank: int, ipc_handles: bytes | None = None, peer_ptrs=None) -> None:
+    ptrs = None
+    if peer_ptrs is not None:
+        ptrs = (C.c_void_p * nranks)(*[C.c_void_p(p) if p else None for p in peer_ptrs])
+    hb = C.c_char_p(ipc_handles) if ipc_handles is not None else None
+    _check(lib().ig_attach_peers(h, int(nranks), int(rank), hb, ptrs), "ig_attach_peers")
+
+
+def peers_from_process_group(handles, group=None) -> None:
+    """Collective: wire the in-kernel NVLink peer exchange of `handles` (one per field, same order
+    on every rank) across the ranks of a torch.distributed group (IPC handles travel through
+    torch.distributed; plumbing only)."""
+    import torch.distributed as dist
+
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    for h in handles:
+        mine = ig_xwin_export(h)
+        allh = [None] * world
+        dist.all_gather_object(allh, mine, group=group)
+        ig_attach_peers(h, world, rank, b"".join(allh))
+    dist.barrier(group=group)
+
+
+def attach_virtual_ranks(handles) -> None:
+    """Wire handles living in ONE process on ONE GPU as ranks of an in-kernel exchange (tests)."""
+    ptrs = [ig_xwin_ptr(h) for h in handles]
+    for r, h in enumerate(handles):
+        ig_attach_peers(h, len(handles), r, None, ptrs)
+
+
 def shard_range(N_total: int, world: int, rank: int):
     """Contiguous DOF range [lo, hi) of `rank` (z-slab partition); sizes differ by <= 1."""
     base, rem = divmod(int(N_total), int(world))
