@@ -58,14 +58,14 @@ template <int MC, int U, class V> struct U2Trip {  // update pass 2
 };
 template <int MC, int U, class V>
 __device__ __forceinline__ void u2trip_load(U2Trip<MC, U, V> &r, const ProjArgs &a, int64_t i0, int64_t stride,
-                                            int64_t nv, int deff) {
+                                            int64_t nv, int deff, unsigned long long pk) {
 #pragma unroll
     for (int u = 0; u < U; ++u) {
         const int64_t i = i0 + u * stride;
         const bool ok = i < nv;
-        r.ax[u] = ok ? ldro<V>(a.Ax, i) : vzero(V());
+        r.ax[u] = ok ? ldp<V>(a.Ax, i, pk) : vzero(V());
 #pragma unroll
-        for (int k = 0; k < MC; ++k) r.col[u][k] = (ok && k < deff) ? ldrw<V>(a.Bt + k * a.ld, i) : vzero(V());
+        for (int k = 0; k < MC; ++k) r.col[u][k] = (ok && k < deff) ? ldp<V>(a.Bt + k * a.ld, i, pk) : vzero(V());
     }
 }
 template <int MC, int U, class V, class CP>
@@ -91,31 +91,32 @@ template <int MC, int U, class V> struct U3Trip {  // update pass 3: U strided e
     V xc[U][SPLIT ? 1 : MC];
 };
 template <int MC, class V>
-__device__ __forceinline__ void u3_load_x(V (&xc)[MC], const ProjArgs &a, int64_t i, bool ok, int nX) {
+__device__ __forceinline__ void u3_load_x(V (&xc)[MC], const ProjArgs &a, int64_t i, bool ok, int nX,
+                                          unsigned long long ps) {
 #pragma unroll
-    for (int k = 0; k < MC; ++k) xc[k] = (ok && k < nX) ? ldrw<V>(a.Xt + k * a.ld, i) : vzero(V());
+    for (int k = 0; k < MC; ++k) xc[k] = (ok && k < nX) ? ldp<V>(a.Xt + k * a.ld, i, ps) : vzero(V());
 }
 // Loads assume the pair is admitted (the common case); if it is not, the prefetched B~/Ax/x
 // values of that one trip are simply unused.
 template <int MC, int U, class V>
 __device__ __forceinline__ void u3trip_load(U3Trip<MC, U, V> &r, const ProjArgs &a, int64_t i0, int64_t stride,
-                                            int64_t nv, int deff, bool rotX, bool adm) {
+                                            int64_t nv, int deff, bool rotX, bool adm, unsigned long long ps) {
     const int nB = adm ? deff : 0;
     const int nX = rotX ? a.M : nB;
 #pragma unroll
     for (int u = 0; u < U; ++u) {
         const int64_t i = i0 + u * stride;
         const bool ok = i < nv;
-        r.ax[u] = (ok && adm) ? ldro<V>(a.Ax, i) : vzero(V());
-        r.xv[u] = (ok && adm) ? ldro<V>(a.x, i) : vzero(V());
+        r.ax[u] = (ok && adm) ? ldp<V>(a.Ax, i, ps) : vzero(V());
+        r.xv[u] = (ok && adm) ? ldp<V>(a.x, i, ps) : vzero(V());
 #pragma unroll
-        for (int k = 0; k < MC; ++k) r.bc[u][k] = (ok && k < nB) ? ldrw<V>(a.Bt + k * a.ld, i) : vzero(V());
-        if constexpr (!U3Trip<MC, U, V>::SPLIT) u3_load_x<MC, V>(r.xc[u], a, i, ok, nX);
+        for (int k = 0; k < MC; ++k) r.bc[u][k] = (ok && k < nB) ? ldp<V>(a.Bt + k * a.ld, i, ps) : vzero(V());
+        if constexpr (!U3Trip<MC, U, V>::SPLIT) u3_load_x<MC, V>(r.xc[u], a, i, ok, nX, ps);
     }
 }
 template <int MC, class V, class CP>
 __device__ __forceinline__ void u3_x_part(const V (&xc)[MC], const ProjArgs &a, int64_t i, bool rotX, V &xt, V &t2,
-                                          CP c1, CP c2, CP gc, CP gs) {
+                                          CP c1, CP c2, CP gc, CP gs, unsigned long long ps) {
     if (rotX) {
         V t = xc[0];
 #pragma unroll
@@ -123,7 +124,7 @@ __device__ __forceinline__ void u3_x_part(const V (&xc)[MC], const ProjArgs &a, 
             if (k < a.M - 1) {
                 V nk;
                 vrot(gc[k], gs[k], t, xc[k + 1], nk);
-                stv<V>(a.Xt + k * a.ld, i, nk);
+                stp<V>(a.Xt + k * a.ld, i, nk, ps);
                 xt = vaxpy(-c1[k], nk, xt);
                 t2 = vaxpy(c2[k], nk, t2);
             }
@@ -139,7 +140,7 @@ __device__ __forceinline__ void u3_x_part(const V (&xc)[MC], const ProjArgs &a, 
 template <int MC, int U, class V, class CP>
 __device__ __forceinline__ void u3trip_store(const U3Trip<MC, U, V> &r, const ProjArgs &a, int64_t i0,
                                              int64_t stride, int64_t nv, int deff, bool rotX, bool adm, double inv,
-                                             CP c1, CP c2, CP gc, CP gs) {
+                                             CP c1, CP c2, CP gc, CP gs, unsigned long long ps) {
 #pragma unroll
     for (int u = 0; u < U; ++u) {
         const int64_t i = i0 + u * stride;
@@ -150,16 +151,16 @@ __device__ __forceinline__ void u3trip_store(const U3Trip<MC, U, V> &r, const Pr
         for (int k = 0; k < MC; ++k) b1 = vaxpy(-c1[k], r.bc[u][k], b1);
 #pragma unroll
         for (int k = 0; k < MC; ++k) s2 = vaxpy(c2[k], r.bc[u][k], s2);
-        if (adm) stv<V>(a.Bt + deff * a.ld, i, vscale(inv, vaxpy(-1.0, s2, b1)));
+        if (adm) stp<V>(a.Bt + deff * a.ld, i, vscale(inv, vaxpy(-1.0, s2, b1)), ps);
         V xt = r.xv[u], t2 = vzero(V());
         if constexpr (U3Trip<MC, U, V>::SPLIT) {
             V xc[MC];
-            u3_load_x<MC, V>(xc, a, i, true, rotX ? a.M : (adm ? deff : 0));
-            u3_x_part<MC, V>(xc, a, i, rotX, xt, t2, c1, c2, gc, gs);
+            u3_load_x<MC, V>(xc, a, i, true, rotX ? a.M : (adm ? deff : 0), ps);
+            u3_x_part<MC, V>(xc, a, i, rotX, xt, t2, c1, c2, gc, gs, ps);
         } else {
-            u3_x_part<MC, V>(r.xc[u], a, i, rotX, xt, t2, c1, c2, gc, gs);
+            u3_x_part<MC, V>(r.xc[u], a, i, rotX, xt, t2, c1, c2, gc, gs, ps);
         }
-        if (adm) stv<V>(a.Xt + deff * a.ld, i, vscale(inv, vaxpy(-1.0, t2, xt)));
+        if (adm) stp<V>(a.Xt + deff * a.ld, i, vscale(inv, vaxpy(-1.0, t2, xt)), ps);
     }
 }
 
@@ -253,6 +254,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_update_fused(ProjArgs a) {
     const bool restart = (a.method == M_PROJ_CLASSIC) && (d >= M);  // Alg. 1 restart
     const int deff = pend ? M - 1 : (restart ? 0 : d);
     const unsigned long long ep1 = c->xepoch[ST_U1] + 1, ep2 = c->xepoch[ST_U2] + 1;
+    const L2Pol pol = make_l2pol();
     if (threadIdx.x < MAXM) {
         const bool rot = pend && threadIdx.x < M - 1;
         s_gc[threadIdx.x] = rot ? c->gc[threadIdx.x] : 1.0;
@@ -280,14 +282,14 @@ __global__ void __launch_bounds__(THREADS, 1) k_update_fused(ProjArgs a) {
     double v[MC + 1];
 #pragma unroll
     for (int k = 0; k <= MC; ++k) v[k] = 0.0;
-    for (int64_t i0 = i_first; i0 < nv; i0 += U * stride) u1_trip<MC, U, V>(a, i0, stride, nv, pend, deff, gc, gs, v);
-    if (tail) u1_trip<MC, 1, double>(a, a.N - 1, 1, a.N, pend, deff, gc, gs, v);
+    for (int64_t i0 = i_first; i0 < nv; i0 += U * stride) u1_trip<MC, U, V>(a, i0, stride, nv, pend, deff, gc, gs, v, pol.keep);
+    if (tail) u1_trip<MC, 1, double>(a, a.N - 1, 1, a.N, pend, deff, gc, gs, v, pol.keep);
     // Serpentine order: pass 2 walks the vectors BACKWARDS, so it starts on the B~/Ax lines pass 1
     // touched last (still in the 126 MB L2); pass 3 walks forwards again and starts on what pass 2
     // touched last.  Same arithmetic per element, fewer HBM bytes per step.
     const int64_t ntrip2 = (i_first < nv) ? (nv - i_first + U * stride - 1) / (U * stride) : 0;
     U2Trip<MC, U, V> pre2;
-    if (deff > 0 && ntrip2 > 0) u2trip_load(pre2, a, i_first + (ntrip2 - 1) * U * stride, stride, nv, deff);
+    if (deff > 0 && ntrip2 > 0) u2trip_load(pre2, a, i_first + (ntrip2 - 1) * U * stride, stride, nv, deff, pol.keep);
     block_partials_store<MC + 1>(v, deff, true, a.blk, sh);
     grid_barrier(&c->bar, 1);
     reduce_all_blocks<MC>(deff, true, a.blk, s_r1);
@@ -305,17 +307,17 @@ __global__ void __launch_bounds__(THREADS, 1) k_update_fused(ProjArgs a) {
         if (ntrip2 > 0) u2trip_compute(pre2, c1, v);
         for (int64_t t = ntrip2 - 2; t >= 0; --t) {
             U2Trip<MC, U, V> r;
-            u2trip_load(r, a, i_first + t * U * stride, stride, nv, deff);
+            u2trip_load(r, a, i_first + t * U * stride, stride, nv, deff, pol.keep);
             u2trip_compute(r, c1, v);
         }
         if (tail) {
             U2Trip<MC, 1, double> r;
-            u2trip_load(r, a, a.N - 1, 1, a.N, deff);
+            u2trip_load(r, a, a.N - 1, 1, a.N, deff, pol.keep);
             u2trip_compute(r, c1, v);
         }
     }
     U3Trip<MC, U3, V> pre3;  // first trip of pass 3, in flight across barrier 2
-    u3trip_load(pre3, a, i_first, stride, nv, deff, pend, true);
+    u3trip_load(pre3, a, i_first, stride, nv, deff, pend, true, pol.stream);
     if (deff > 0) block_partials_store<MC + 1>(v, deff, true, a.blk + BLK2, sh);
     grid_barrier(&c->bar, 2);
     if (deff > 0) reduce_all_blocks<MC>(deff, true, a.blk + BLK2, s_r2);
@@ -346,16 +348,16 @@ __global__ void __launch_bounds__(THREADS, 1) k_update_fused(ProjArgs a) {
     }
     // ---- pass 3: [Givens rotation of X~] + store the admitted pair
     if (adm || pend) {
-        u3trip_store(pre3, a, i_first, stride, nv, deff, pend, adm, inv, c1, c2, gc, gs);
+        u3trip_store(pre3, a, i_first, stride, nv, deff, pend, adm, inv, c1, c2, gc, gs, pol.stream);
         for (int64_t i0 = i_first + U3 * stride; i0 < nv; i0 += U3 * stride) {
             U3Trip<MC, U3, V> r;
-            u3trip_load(r, a, i0, stride, nv, deff, pend, adm);
-            u3trip_store(r, a, i0, stride, nv, deff, pend, adm, inv, c1, c2, gc, gs);
+            u3trip_load(r, a, i0, stride, nv, deff, pend, adm, pol.stream);
+            u3trip_store(r, a, i0, stride, nv, deff, pend, adm, inv, c1, c2, gc, gs, pol.stream);
         }
         if (tail) {
             U3Trip<MC, 1, double> r;
-            u3trip_load(r, a, a.N - 1, 1, a.N, deff, pend, adm);
-            u3trip_store(r, a, a.N - 1, 1, a.N, deff, pend, adm, inv, c1, c2, gc, gs);
+            u3trip_load(r, a, a.N - 1, 1, a.N, deff, pend, adm, pol.stream);
+            u3trip_store(r, a, a.N - 1, 1, a.N, deff, pend, adm, inv, c1, c2, gc, gs, pol.stream);
         }
     }
     pdl_trigger();
