@@ -18,6 +18,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_extrap(const __grid_constant__ E
     // accumulation order is oldest -> newest, like Eq. EXTRAPEXPN.
     typedef typename std::conditional<VEC == 2, double2, double>::type V;
     pdl_wait();
+    // (an L2 evict_first hint on these single-use loads measured 8% SLOWER at N = 2^27: not used)
     const int f = a.f;
     const int64_t nv = a.N / VEC;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;

@@ -31,12 +31,12 @@ template <int MC, int U, class V> struct XTrip {  // form pass 2: U strided elem
 };
 template <int MC, int U, class V>
 __device__ __forceinline__ void xtrip_load(XTrip<MC, U, V> &r, const ProjArgs &a, int64_t i0, int64_t stride,
-                                           int64_t nv, int d) {
+                                           int64_t nv, int d, unsigned long long ps) {
 #pragma unroll
     for (int u = 0; u < U; ++u) {
         const int64_t i = i0 + u * stride;
 #pragma unroll
-        for (int k = 0; k < MC; ++k) r.col[u][k] = (i < nv && k < d) ? ldro<V>(a.Xt + k * a.ld, i) : vzero(V());
+        for (int k = 0; k < MC; ++k) r.col[u][k] = (i < nv && k < d) ? ldp<V>(a.Xt + k * a.ld, i, ps) : vzero(V());
     }
 }
 template <int MC, int U, class V>
@@ -175,6 +175,9 @@ __global__ void __launch_bounds__(THREADS, 1) k_form_fused(ProjArgs a) {
     const int d = c->d;
     if (d == 0) return;  // uniform: x0 stays the caller's fallback
     const unsigned long long ep = c->xepoch[ST_FORM] + 1;
+    // All form traffic is single-use within the call (the caller's solve runs next): evict_first,
+    // so the guess does not push the solver's working set out of L2.
+    const unsigned long long ps = make_l2pol().stream;
     const int64_t nv = a.N / VEC;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     const int64_t i_first = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -188,9 +191,9 @@ __global__ void __launch_bounds__(THREADS, 1) k_form_fused(ProjArgs a) {
         for (int u = 0; u < U; ++u) {
             const int64_t i = i0 + u * stride;
             const bool ok = i < nv;
-            bv[u] = ok ? ldro<V>(a.b, i) : vzero(V());
+            bv[u] = ok ? ldp<V>(a.b, i, ps) : vzero(V());
 #pragma unroll
-            for (int k = 0; k < MC; ++k) col[u][k] = (ok && k < d) ? ldro<V>(a.Bt + k * a.ld, i) : vzero(V());
+            for (int k = 0; k < MC; ++k) col[u][k] = (ok && k < d) ? ldp<V>(a.Bt + k * a.ld, i, ps) : vzero(V());
         }
 #pragma unroll
         for (int u = 0; u < U; ++u)
@@ -205,7 +208,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_form_fused(ProjArgs a) {
             if (k < d) v[k] = fma(a.Bt[k * a.ld + i], bv, v[k]);
     }
     XTrip<MC, U, V> pre;  // first trip of pass 2, in flight across the barrier
-    xtrip_load(pre, a, i_first, stride, nv, d);
+    xtrip_load(pre, a, i_first, stride, nv, d, ps);
     block_partials_store<MC + 1>(v, d, false, a.blk, sh);
     grid_barrier(&c->bar, 1);
     reduce_all_blocks<MC>(d, false, a.blk, s_red);
@@ -217,7 +220,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_form_fused(ProjArgs a) {
     xtrip_store(pre, a, i_first, stride, nv, al);
     for (int64_t i0 = i_first + U * stride; i0 < nv; i0 += U * stride) {
         XTrip<MC, U, V> r;
-        xtrip_load(r, a, i0, stride, nv, d);
+        xtrip_load(r, a, i0, stride, nv, d, ps);
         xtrip_store(r, a, i0, stride, nv, al);
     }
     if (VEC == 2 && (a.N & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
