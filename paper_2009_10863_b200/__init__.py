@@ -20,6 +20,8 @@ from .ig import (  # noqa: F401
     ig_comm_unique_id,
     ig_copy_history,
     ig_create,
+    ig_create_ext,
+    ig_storage_bytes,
     ig_destroy,
     ig_form_guess,
     ig_form_guess_host,

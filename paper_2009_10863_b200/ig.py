@@ -71,6 +71,23 @@ def ig_create(N: int, method: int, m: int, degree: int = 0, stream=None):
     return h
 
 
+def ig_storage_bytes(N: int, method: int, m: int) -> int:
+    return int(lib().ig_storage_bytes(int(N), int(method), int(m)))
+
+
+def ig_create_ext(N: int, method: int, m: int, degree: int, storage, stream=None):
+    """Handle whose history slabs live in caller-owned device memory (e.g. a torch uint8/fp64 tensor)."""
+    if not isinstance(storage, torch.Tensor) or not storage.is_cuda or not storage.is_contiguous():
+        raise TypeError("storage must be a contiguous CUDA tensor")
+    nbytes = storage.numel() * storage.element_size()
+    h = lib().ig_create_ext(int(N), int(method), int(m), int(degree), C.c_void_p(storage.data_ptr()), nbytes)
+    if not h:
+        raise IGError(IG_E_ARG, "ig_create_ext")
+    s = stream if stream is not None else torch.cuda.current_stream()
+    _check(lib().ig_set_stream(h, C.c_void_p(s.cuda_stream)), "ig_set_stream")
+    return h
+
+
 def ig_destroy(h) -> None:
     lib().ig_destroy(h)
 
@@ -279,10 +296,14 @@ class InitialGuess:
     """One history space (one field).  Thin wrapper over an ig_t handle."""
 
     def __init__(self, N: int, method="proj_qr", m: int = 8, degree: int = 0, eps: float | None = None,
-                 comm=None, stream=None, fused: bool = True):
+                 comm=None, stream=None, fused: bool = True, storage=None):
         self.N, self.m, self.degree = int(N), int(m), int(degree)
         self.method = METHODS[method] if isinstance(method, str) else int(method)
-        self.h = ig_create(self.N, self.method, self.m, self.degree, stream)
+        self.storage = storage  # keep caller-provided history memory alive with the handle
+        if storage is None:
+            self.h = ig_create(self.N, self.method, self.m, self.degree, stream)
+        else:
+            self.h = ig_create_ext(self.N, self.method, self.m, self.degree, storage, stream)
         if eps is not None:
             ig_set_admit_tol(self.h, eps)
         if not fused:

@@ -383,3 +383,28 @@ def test_projection_step_is_graph_capturable(fused):
         ora.update(x, Ax)
         assert ig.d == ora.d
     ig.close()
+
+
+def test_history_in_caller_storage():
+    """ig_create_ext: the history slabs live in a torch-owned allocation (caching allocator)."""
+    from paper_2009_10863_b200 import IG_EXTRAP_LS, IG_PROJ_QR, InitialGuess, ig_storage_bytes
+
+    g = Grid(30, 2)
+    seq = _seq(g, 12, dt=1e-2)
+    M = 5
+    sp = torch.empty(ig_storage_bytes(g.N, IG_PROJ_QR, M), dtype=torch.uint8, device="cuda")
+    se = torch.empty(ig_storage_bytes(g.N, IG_EXTRAP_LS, M), dtype=torch.uint8, device="cuda")
+    hp = InitialGuess(g.N, "proj_qr", M, storage=sp)
+    he = InitialGuess(g.N, "extrap_ls", M, 2, storage=se)
+    op, oe = ProjQR(g.N, M), ExtrapLS(g.N, M, 2)
+    for b, x, Ax in seq:
+        for o, h in ((op, hp), (oe, he)):
+            x0 = torch.zeros(g.N, dtype=torch.float64, device="cuda")
+            h.form_guess(torch.from_numpy(b).cuda(), x0)
+            assert _rel(x0.cpu().numpy(), o.form_guess(b, np.zeros(g.N))) <= TOL
+            o.update(x, Ax)
+            h.update(torch.from_numpy(x).cuda(), torch.from_numpy(Ax).cuda())
+    hp.close()
+    he.close()
+    with pytest.raises(Exception):
+        InitialGuess(g.N, "proj_qr", M, storage=sp[:100])  # too small -> IG_E_ARG
