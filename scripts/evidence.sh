@@ -14,3 +14,6 @@ KREGEX="k_update_fused|k_form_fused|k_extrap|k_copy" SKIP=40 COUNT=4 bash script
 python scripts/summarize_ncu.py --launches gpurun_out/launches.csv --full gpurun_out/prof.ncu-rep --bench gpurun_out/bench.log --tag ${TAG} > gpurun_out/summary.log 2>&1
 cp -r profiles gpurun_out/profiles_new
 for f in pytest_gpu smoke bench bench_ref; do tail -n 2 gpurun_out/$f.log; done
+timeout 1200 python scripts/bench_sweep.py --out gpurun_out/profiles_new/${TAG}_sweep.md > gpurun_out/sweep.log 2>&1
+bash scripts/sanitize.sh > gpurun_out/sanitize_summary.txt 2>&1
+cp gpurun_out/sanitize_summary.txt gpurun_out/profiles_new/${TAG}_sanitize_summary.txt
