@@ -47,6 +47,8 @@ def parse():
     p.add_argument("--e2e-steps", type=int, default=20)
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-seconds", type=float, default=15.0, help="budget of the oracle cpu_baseline sample")
+    p.add_argument("--same-gpu", action="store_true",
+                   help="TEST MODE: all ranks on GPU 0 (gloo plumbing, 1/N of the SMs each) to exercise the N>1 path")
     p.add_argument("--exchange", choices=["peer", "nccl"], default="peer",
                    help="N>1 projection sums: in-kernel NVLink peer exchange (fused) or NCCL between kernels")
     return p.parse_args()
@@ -135,10 +137,12 @@ def dist_setup(args):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if args.gpus != world and world > 1:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    if args.same_gpu:
+        local = 0
     if torch.cuda.is_available():
         torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl" if torch.cuda.is_available() else "gloo")
+        dist.init_process_group("nccl" if (torch.cuda.is_available() and not args.same_gpu) else "gloo")
     return world, rank, local
 
 
@@ -148,7 +152,8 @@ def max_over_ranks(v: float, world: int) -> float:
     import torch
     import torch.distributed as dist
 
-    t = torch.tensor([v], dtype=torch.float64, device="cuda")
+    dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+    t = torch.tensor([v], dtype=torch.float64, device=dev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 
@@ -258,6 +263,10 @@ def run_ours(args, world, rank, local):
     comm = comm_from_process_group() if (world > 1 and args.exchange == "nccl") else None
     hp = InitialGuess(N, "proj_qr", M, comm=comm)
     if world > 1 and args.exchange == "peer":
+        if args.same_gpu:  # ranks share one GPU: each persistent kernel gets 1/world of the SMs
+            from paper_2009_10863_b200 import ig_set_grid_limit
+
+            ig_set_grid_limit(hp.h, torch.cuda.get_device_properties(dev).multi_processor_count // world)
         peers_from_process_group([hp.h])
     he = InitialGuess(N, "extrap_ls", M, p)
     x0p = torch.zeros(N, dtype=torch.float64, device=dev)
@@ -387,7 +396,8 @@ def run_ours(args, world, rank, local):
                           "l2": f"fresh inputs every step; per-step working set "
                                 f"{(2 * M + M + 5) * 8 * N / 1e9:.2f} GB > L2 126 MB",
                           "parallelism": f"dof-shard{world}" if world > 1 else "single",
-                          "exchange": (args.exchange if world > 1 else "none")},
+                          "exchange": (args.exchange if world > 1 else "none"),
+                          "mode": "TEST: all ranks on one GPU" if args.same_gpu else "one rank per GPU"},
                "gpu_launches": launches, "roofline": roofline, "kernels": kernels,
                "clocks": sampler.summary(), "e2e": e2e, "cpu_baseline": cpu,
                "proj_state": {"d": st["d"], "rho_last": st["rho"]}, "host_enqueue_us_per_step": host_us}
