@@ -11,6 +11,7 @@
 //                    [X~ downdate + x~, b~, admission, new columns] --exit--> control block
 // The element arithmetic is the same device code as the one-kernel-per-pass path
 // (proj_common.cuh), which stays in use when partial sums must cross ranks (G > 1).
+#include <cstdlib>
 #include <type_traits>
 
 #include "proj_common.cuh"
@@ -405,6 +406,18 @@ template <class K> static cudaError_t coop_launch(K kern, const ProjArgs &a, int
     if (occ < 1) return cudaErrorInvalidConfiguration;
     if (occ > 4) occ = 4;
     int grid = nsm * occ;
+    // Optional (IG_MIN_TRIPS): fewer CTAs for small vectors (>= that many grid-stride trips per
+    // thread).  Measured: it only slows small N down (1e5 DOFs, QR(8): 27.7 us at 1 CTA/SM vs
+    // 33.9 us at 4 trips/thread) -- the per-call cost there is latency, not barrier width.
+    static const int min_trips = [] {
+        const char *e = getenv("IG_MIN_TRIPS");
+        return e ? atoi(e) : 0;
+    }();
+    if (min_trips > 0) {
+        const int64_t nv = a.N / 2;
+        const int64_t want = (nv + (int64_t)THREADS * min_trips - 1) / ((int64_t)THREADS * min_trips);
+        if (want < grid) grid = want < 1 ? 1 : (int)want;
+    }
     if (a.max_grid > 0 && grid > a.max_grid) grid = a.max_grid;
     if (grid > MAXB) grid = MAXB;
     return launch_ex(kern, grid, s, true, a);
