@@ -158,6 +158,10 @@ void *ig_xwin_ptr(ig_t h);
 int ig_attach_peers(ig_t h, int nranks, int rank, const void *ipc_handles, void *const *peer_ptrs);
 /* Cap the grid of the persistent kernels (0 = SMs x occupancy). */
 int ig_set_grid_limit(ig_t h, int max_blocks);
+/* Failure detection: a grid barrier or peer-exchange wait longer than `seconds` (default 10) gives
+ * up instead of hanging the GPU and records the event; the next ig_get_stats / ig_history_dim
+ * returns IG_E_STATE (the history is then invalid: ig_reset every rank). */
+int ig_set_watchdog(ig_t h, double seconds);
 
 /* ---------------------------------------------------------------- introspection (tests/bench) */
 

@@ -40,6 +40,7 @@ from .ig import (  # noqa: F401
     ig_weights,
     shard_range,
     ig_set_grid_limit,
+    ig_set_watchdog,
     ig_xwin_export,
     ig_xwin_ptr,
     ig_attach_peers,

@@ -138,6 +138,7 @@ struct ig_ctx {
     bool fused = true;  // persistent fused kernels when G == 1 (ig_set_schedule)
     ig_comm_ctx *comm = nullptr;
     int max_grid = 0;   // ig_set_grid_limit
+    unsigned long long watchdog_ns = WATCHDOG_NS;  // ig_set_watchdog
     // in-kernel peer exchange (ig_attach_peers)
     XWin *xwin = nullptr;
     Exchange xc = {};
@@ -243,6 +244,7 @@ ProjArgs proj_args(ig_t h) {
     a.gath = h->gath;
     a.G = h->G;
     a.max_grid = h->max_grid;
+    a.watchdog_ns = h->watchdog_ns;
     a.xc = h->xc;
     return a;
 }
@@ -635,6 +637,12 @@ int ig_attach_comm(ig_t h, ig_comm_t c) {
     return IG_OK;
 }
 
+int ig_set_watchdog(ig_t h, double seconds) {
+    if (!h || !(seconds > 0.0)) return set_err(IG_E_ARG, "bad handle or watchdog time");
+    h->watchdog_ns = (unsigned long long)(seconds * 1e9);
+    return IG_OK;
+}
+
 int ig_set_grid_limit(ig_t h, int max_blocks) {
     if (!h || max_blocks < 0) return set_err(IG_E_ARG, "bad handle or grid limit");
     h->max_grid = max_blocks;
@@ -702,12 +710,25 @@ int ig_attach_peers(ig_t h, int nranks, int rank, const void *ipc_handles, void 
     return IG_OK;
 }
 
+static int watchdog_error(int err) {
+    if (err == 1)
+        return set_err(IG_E_STATE, "device watchdog: a grid barrier timed out (persistent grid not co-resident?); "
+                                   "the history is invalid, ig_reset the handle");
+    if (err == 2)
+        return set_err(IG_E_STATE, "device watchdog: the peer exchange timed out (a rank stopped calling?); "
+                                   "the history is invalid, ig_reset every rank");
+    return IG_OK;
+}
+
 int ig_history_dim(ig_t h, int *d) {
     if (!h || !d) return set_err(IG_E_ARG, "NULL argument");
     DevGuard g(h->dev);
     if (is_proj(h->method)) {
-        CUDA_OK(cudaMemcpyAsync(d, &h->ctrl->d, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
+        Ctrl c;  // the leading ints (d ... err)
+        CUDA_OK(cudaMemcpyAsync(&c, h->ctrl, offsetof(Ctrl, ticket), cudaMemcpyDeviceToHost, h->stream));
         CUDA_OK(cudaStreamSynchronize(h->stream));
+        *d = c.d;
+        return watchdog_error(c.err);
     } else {
         *d = h->fill;
     }
@@ -737,6 +758,7 @@ int ig_get_stats(ig_t h, ig_stats_t *out) {
         out->rho = c.rho;
         out->norm_Ax = c.nAx;
         out->norm_bt = c.nb;
+        if (c.err) return watchdog_error(c.err);
     } else {
         out->d = h->fill;
         out->admitted = 1;

@@ -17,6 +17,7 @@ constexpr int THREADS = 256;   // threads per block of every streaming kernel
 
 enum Stage { ST_FORM = 0, ST_U1 = 1, ST_U2 = 2, ST_U3 = 3, NSTAGE = 4 };
 constexpr int MAXG = 8;        // ranks of an in-kernel peer-memory exchange (one NVLink node)
+constexpr unsigned long long WATCHDOG_NS = 10ull * 1000 * 1000 * 1000;  // spin-wait limit (10 s)
 
 // Exchange window of one rank, written by every rank over NVLink peer memory (or, for ranks in
 // one process, ordinary device memory): data[stage][epoch parity][sender][slot] and a monotonic
@@ -43,6 +44,7 @@ struct Ctrl {
     int deff;       // dimension the Gram-Schmidt passes of the current update use
     int admitted;   // last update admitted its pair
     int last_rot;   // the last update applied a downdate (bytes accounting)
+    int err;        // device watchdog: 0 ok, 1 grid-barrier timeout, 2 peer-exchange timeout
     unsigned ticket[NSTAGE];
     unsigned bar, bar_exit;        // grid barrier / exit counters of the fused kernels
     unsigned long long xepoch[NSTAGE];  // completed peer exchanges per stage (all ranks agree)
@@ -70,6 +72,7 @@ struct ProjArgs {
     const double *x;       // update: solution
     const double *Ax;      // update: A x
     int max_grid;          // cap on the persistent kernels' grid (0: SMs x occupancy)
+    unsigned long long watchdog_ns;  // spin-wait limit of grid barriers / peer exchange
     Exchange xc;           // in-kernel peer exchange (xc.G > 1) for the fused kernels
 };
 

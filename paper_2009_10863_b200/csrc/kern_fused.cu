@@ -211,9 +211,9 @@ __global__ void __launch_bounds__(THREADS, 1) k_form_fused(ProjArgs a) {
     XTrip<MC, U, V> pre;  // first trip of pass 2, in flight across the barrier
     xtrip_load(pre, a, i_first, stride, nv, d, ps);
     block_partials_store<MC + 1>(v, d, false, a.blk, sh);
-    grid_barrier(&c->bar, 1);
+    grid_barrier(&c->bar, 1, &c->err, a.watchdog_ns);
     reduce_all_blocks<MC>(d, false, a.blk, s_red);
-    if (a.xc.G > 1) peer_allreduce(a.xc, ST_FORM, d, false, s_red, ep);
+    if (a.xc.G > 1) peer_allreduce(a.xc, ST_FORM, d, false, s_red, ep, &c->err, a.watchdog_ns);
     double al[MC];
 #pragma unroll
     for (int k = 0; k < MC; ++k) al[k] = (k < d) ? s_red[k] : 0.0;
@@ -295,9 +295,9 @@ __global__ void __launch_bounds__(THREADS, 1) k_update_fused(ProjArgs a) {
     U2Trip<MC, U, V> pre2;
     if (deff > 0 && ntrip2 > 0) u2trip_load(pre2, a, i_first + (ntrip2 - 1) * U * stride, stride, nv, deff, pol.keep);
     block_partials_store<MC + 1>(v, deff, true, a.blk, sh);
-    grid_barrier(&c->bar, 1);
+    grid_barrier(&c->bar, 1, &c->err, a.watchdog_ns);
     reduce_all_blocks<MC>(deff, true, a.blk, s_r1);
-    if (a.xc.G > 1) peer_allreduce(a.xc, ST_U1, deff, true, s_r1, ep1);
+    if (a.xc.G > 1) peer_allreduce(a.xc, ST_U1, deff, true, s_r1, ep1, &c->err, a.watchdog_ns);
     if (threadIdx.x < MAXM) s_c1[threadIdx.x] = (threadIdx.x < deff) ? s_r1[threadIdx.x] : 0.0;
     __syncthreads();
     if constexpr (!SMC) {
@@ -323,9 +323,9 @@ __global__ void __launch_bounds__(THREADS, 1) k_update_fused(ProjArgs a) {
     U3Trip<MC, U3, V> pre3;  // first trip of pass 3, in flight across barrier 2
     u3trip_load(pre3, a, i_first, stride, nv, deff, pend, true, pol.stream);
     if (deff > 0) block_partials_store<MC + 1>(v, deff, true, a.blk + BLK2, sh);
-    grid_barrier(&c->bar, 2);
+    grid_barrier(&c->bar, 2, &c->err, a.watchdog_ns);
     if (deff > 0) reduce_all_blocks<MC>(deff, true, a.blk + BLK2, s_r2);
-    if (deff > 0 && a.xc.G > 1) peer_allreduce(a.xc, ST_U2, deff, true, s_r2, ep2);
+    if (deff > 0 && a.xc.G > 1) peer_allreduce(a.xc, ST_U2, deff, true, s_r2, ep2, &c->err, a.watchdog_ns);
     if (threadIdx.x == 0) {
         const double nAx2 = s_r1[NORM];
         double nb2;

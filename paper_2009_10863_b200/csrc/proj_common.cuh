@@ -198,13 +198,31 @@ __device__ __forceinline__ unsigned ld_acquire_u32(const unsigned *p) {
 // monotonically within one launch; barrier number `phase` (1, 2, ...) waits for phase*gridDim
 // arrivals.  The last CTA to leave the kernel resets the counters (grid_exit), so the next launch
 // (stream-ordered) starts from zero: safe under CUDA-graph replay.
-__device__ __forceinline__ void grid_barrier(unsigned *ctr, unsigned phase) {
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+// Failure detection: a spin that exceeds WATCHDOG_NS (grid not co-resident, a peer rank that
+// stopped calling) records a code in the control block and gives up instead of hanging the GPU;
+// the host reports IG_E_STATE at the next synchronising call (ig_get_stats / ig_history_dim).
+__device__ __forceinline__ void watchdog_trip(int *err, int code) { atomicCAS(err, 0, code); }
+
+__device__ __forceinline__ void grid_barrier(unsigned *ctr, unsigned phase, int *err, unsigned long long limit) {
     __syncthreads();
     if (threadIdx.x == 0) {
         __threadfence();
         atomicAdd(ctr, 1u);
         const unsigned target = phase * gridDim.x;
-        while (ld_acquire_u32(ctr) < target) __nanosleep(20);
+        const unsigned long long t0 = globaltimer_ns();
+        while (ld_acquire_u32(ctr) < target) {
+            __nanosleep(20);
+            if (globaltimer_ns() - t0 > limit) {
+                watchdog_trip(err, 1);
+                break;
+            }
+        }
         __threadfence();
     }
     __syncthreads();
@@ -257,7 +275,7 @@ __device__ __forceinline__ double ld_relaxed_sys_f64(const double *p) {
 // acquires all G flags and sums the G contributions in RANK ORDER, so all ranks (and all CTAs)
 // get bitwise-identical results.  `buf` is overwritten with the global sums.
 __device__ __forceinline__ void peer_allreduce(const Exchange &xc, int stage, int nc, bool norm, double *buf,
-                                               unsigned long long epoch) {
+                                               unsigned long long epoch, int *err, unsigned long long limit) {
     const int par = (int)(epoch & 1ull);
     const int G = xc.G, me = xc.rank;
     if (blockIdx.x == 0) {
@@ -272,8 +290,15 @@ __device__ __forceinline__ void peer_allreduce(const Exchange &xc, int stage, in
     }
     if (threadIdx.x == 0) {
         const XWin *w = xc.peer[me];
+        const unsigned long long t0 = globaltimer_ns();
         for (int r = 0; r < G; ++r)
-            while (ld_acquire_sys_u64(&w->flag[stage][r]) < epoch) __nanosleep(32);
+            while (ld_acquire_sys_u64(&w->flag[stage][r]) < epoch) {
+                __nanosleep(32);
+                if (globaltimer_ns() - t0 > limit) {
+                    watchdog_trip(err, 2);
+                    break;
+                }
+            }
     }
     __syncthreads();
     for (int k = threadIdx.x; k < PS; k += blockDim.x) {

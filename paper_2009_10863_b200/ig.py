@@ -241,6 +241,10 @@ def ig_set_grid_limit(h, max_blocks: int) -> None:
     _check(lib().ig_set_grid_limit(h, int(max_blocks)), "ig_set_grid_limit")
 
 
+def ig_set_watchdog(h, seconds: float) -> None:
+    _check(lib().ig_set_watchdog(h, float(seconds)), "ig_set_watchdog")
+
+
 def ig_xwin_export(h) -> bytes:
     buf = (C.c_char * 64)()
     _check(lib().ig_xwin_export(h, buf), "ig_xwin_export")

@@ -63,3 +63,23 @@ def test_virtual_ranks_match_unsharded_oracle(G, M, method):
         assert len({(s["admitted"], s["rho"]) for s in st}) == 1  # bitwise-identical decisions
     for ig in igs:
         ig.close()
+
+
+@pytest.mark.timeout(120)
+def test_watchdog_reports_a_missing_rank():
+    """Failure detection: rank 1 never calls; rank 0's in-kernel exchange gives up after the
+    watchdog time instead of hanging, and the host reports IG_E_STATE."""
+    from paper_2009_10863_b200 import IGError, InitialGuess, attach_virtual_ranks, ig_set_grid_limit, ig_set_watchdog
+
+    N = 1000
+    igs = [InitialGuess(N, "proj_qr", 4) for _ in range(2)]
+    for ig in igs:
+        ig_set_grid_limit(ig.h, 8)
+        ig_set_watchdog(ig.h, 0.2)
+    attach_virtual_ranks([ig.h for ig in igs])
+    x = torch.rand(N, dtype=torch.float64, device="cuda")
+    igs[0].update(x, x)  # only rank 0 participates
+    with pytest.raises(IGError, match="watchdog"):
+        igs[0].stats()
+    for ig in igs:
+        ig.close()
