@@ -267,7 +267,13 @@ def run_ours(args, world, rank, local):
             from paper_2009_10863_b200 import ig_set_grid_limit
 
             ig_set_grid_limit(hp.h, torch.cuda.get_device_properties(dev).multi_processor_count // world)
-        peers_from_process_group([hp.h])
+        try:
+            peers_from_process_group([hp.h])
+        except RuntimeError as e:  # no P2P between the GPUs: fall back to NCCL between kernels
+            print(f"[bench] peer exchange unavailable ({e}); using NCCL", file=sys.stderr, flush=True)
+            args.exchange = "nccl"
+            hp.close()
+            hp = InitialGuess(N, "proj_qr", M, comm=comm_from_process_group())
     he = InitialGuess(N, "extrap_ls", M, p)
     x0p = torch.zeros(N, dtype=torch.float64, device=dev)
     x0e = torch.zeros(N, dtype=torch.float64, device=dev)

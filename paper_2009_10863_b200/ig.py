@@ -273,12 +273,26 @@ def peers_from_process_group(handles, group=None) -> None:
     import torch.distributed as dist
 
     rank, world = dist.get_rank(group), dist.get_world_size(group)
+    dev = torch.cuda.current_device()
+    devs = [None] * world
+    dist.all_gather_object(devs, (socket_host(), dev), group=group)
+    for host, d in devs:
+        if host != socket_host():
+            raise RuntimeError("the in-kernel peer exchange needs all ranks on one node")
+        if d != dev and not torch.cuda.can_device_access_peer(dev, d):
+            raise RuntimeError(f"GPU {dev} cannot access GPU {d} (no P2P/NVLink): use the NCCL exchange")
     for h in handles:
         mine = ig_xwin_export(h)
         allh = [None] * world
         dist.all_gather_object(allh, mine, group=group)
         ig_attach_peers(h, world, rank, b"".join(allh))
     dist.barrier(group=group)
+
+
+def socket_host() -> str:
+    import socket
+
+    return socket.gethostname()
 
 
 def attach_virtual_ranks(handles) -> None:
