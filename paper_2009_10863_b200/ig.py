@@ -276,11 +276,17 @@ def peers_from_process_group(handles, group=None) -> None:
     dev = torch.cuda.current_device()
     devs = [None] * world
     dist.all_gather_object(devs, (socket_host(), dev), group=group)
+    why = None
     for host, d in devs:
         if host != socket_host():
-            raise RuntimeError("the in-kernel peer exchange needs all ranks on one node")
-        if d != dev and not torch.cuda.can_device_access_peer(dev, d):
-            raise RuntimeError(f"GPU {dev} cannot access GPU {d} (no P2P/NVLink): use the NCCL exchange")
+            why = "the in-kernel peer exchange needs all ranks on one node"
+        elif d != dev and not torch.cuda.can_device_access_peer(dev, d):
+            why = f"GPU {dev} cannot access GPU {d} (no P2P/NVLink)"
+    verdicts = [None] * world
+    dist.all_gather_object(verdicts, why, group=group)  # every rank takes the same decision
+    bad = [v for v in verdicts if v]
+    if bad:
+        raise RuntimeError(bad[0] + ": use the NCCL exchange")
     for h in handles:
         mine = ig_xwin_export(h)
         allh = [None] * world
