@@ -115,6 +115,14 @@ int ig_form_guess(ig_t h, const double *b, double *x0);
  *     x == ig_next_slot(h) nothing is copied; otherwise one copy. */
 int ig_update(ig_t h, const double *x, const double *Ax);
 
+/* Multi-field batch (one history space per field): handles[i] with b[i], x0[i].
+ * Consecutive extrapolation handles on the same device and stream (up to 4) share ONE kernel
+ * launch; projection handles run their own persistent kernel.  bs may be NULL if all handles are
+ * extrapolation; Axs may be NULL if no handle is a projection.  Same semantics per field as the
+ * single-handle calls. */
+int ig_form_guess_batch(int n, ig_t *handles, const double *const *bs, double *const *x0s);
+int ig_update_batch(int n, ig_t *handles, const double *const *xs, const double *const *Axs);
+
 /* Host-buffer variants (end-to-end path): inputs are copied host->device into handle-owned
  * staging buffers on the stream, the result device->host; these SYNC before returning.
  *   ig_form_guess_host: x0 (in: fallback, out: guess) and b are host arrays of N doubles.

@@ -263,6 +263,31 @@ int exchange(ig_t h, int stage) {
 }
 
 int slot_index(ig_t h, int j) { return (h->head + j) % h->M; }  // j-th oldest stored solution
+
+// Extrapolation kernel arguments for the current fill; false when there is nothing to do.
+// Only nonzero weights are streamed (exact zeros contribute exactly nothing): SPEXTRAP reads its
+// m+1 selected solutions (Table 1: (m+2)N), LS skips e.g. beta_4 = 0 of EXTRAP(3,8).
+bool extrap_args(ig_t h, double *x0, ExtrapArgs &a, bool &aligned) {
+    const int f = h->fill < h->M ? h->fill : h->M;
+    h->last_form_f = 0;
+    if (f == 0) return false;
+    memset(&a, 0, sizeof a);
+    a.N = h->N;
+    a.x0 = x0;
+    aligned = al16(x0);
+    int nz = 0;
+    for (int j = 0; j < f; ++j) {
+        const double bj = h->table[f - 1][j];
+        if (bj == 0.0) continue;
+        a.src[nz] = h->slots[slot_index(h, j)];
+        a.beta[nz] = bj;
+        aligned = aligned && al16(a.src[nz]);
+        ++nz;
+    }
+    a.f = nz;
+    h->last_form_f = nz;
+    return true;
+}
 double *next_slot_ptr(ig_t h) { return h->fill < h->M ? h->slots[slot_index(h, h->fill)] : h->slots[h->head]; }
 
 ig_t create_impl(int64_t N, int method, int m, int degree, void *storage, size_t bytes) {
@@ -434,28 +459,9 @@ int ig_form_guess(ig_t h, const double *b, double *x0) {
         count(h, 2);
         return IG_OK;
     }
-    const int f = h->fill < h->M ? h->fill : h->M;
-    h->last_form_f = f;
-    if (f == 0) return IG_OK;  // x0 untouched (AMB-13)
     ExtrapArgs a;
-    memset(&a, 0, sizeof a);
-    a.f = f;
-    a.N = h->N;
-    a.x0 = x0;
-    // Only nonzero weights are streamed (exact zeros contribute exactly nothing): SPEXTRAP reads
-    // its m+1 selected solutions (Table 1: (m+2)N), LS skips e.g. beta_4 = 0 of EXTRAP(3,8).
-    bool aligned = al16(x0);
-    int nz = 0;
-    for (int j = 0; j < f; ++j) {
-        const double bj = h->table[f - 1][j];
-        if (bj == 0.0) continue;
-        a.src[nz] = h->slots[slot_index(h, j)];
-        a.beta[nz] = bj;
-        aligned = aligned && al16(a.src[nz]);
-        ++nz;
-    }
-    a.f = nz;
-    h->last_form_f = nz;
+    bool aligned = true;
+    if (!extrap_args(h, x0, a, aligned)) return IG_OK;  // fill == 0: x0 untouched (AMB-13)
     {
         Prof p(h, IG_K_EXTRAP);
         CUDA_OK(launch_extrap(a, aligned ? 2 : 1, h->nsm, h->stream));
@@ -508,6 +514,53 @@ int ig_update(ig_t h, const double *x, const double *Ax) {
     }
     if (h->fill < h->M) ++h->fill;
     else h->head = (h->head + 1) % h->M;
+    return IG_OK;
+}
+
+int ig_form_guess_batch(int n, ig_t *hs, const double *const *bs, double *const *x0s) {
+    if (n < 0 || (n > 0 && (!hs || !x0s))) return set_err(IG_E_ARG, "bad batch arguments");
+    int i = 0;
+    while (i < n) {
+        ig_t h = hs[i];
+        if (!h) return set_err(IG_E_ARG, "NULL handle in batch");
+        if (!is_extrap(h->method)) {  // projection: its own persistent kernel
+            int rc = ig_form_guess(h, bs ? bs[i] : nullptr, x0s[i]);
+            if (rc) return rc;
+            ++i;
+            continue;
+        }
+        // group consecutive extrapolation handles on the same device and stream
+        ExtrapBatch b;
+        memset(&b, 0, sizeof b);
+        bool aligned = true;
+        int j = i;
+        for (; j < n && b.nf < MAXF; ++j) {
+            ig_t q = hs[j];
+            if (!q || !is_extrap(q->method) || q->dev != h->dev || q->stream != h->stream) break;
+            if (!x0s[j]) return set_err(IG_E_ARG, "x0 is NULL");
+            bool al = true;
+            if (extrap_args(q, x0s[j], b.f[b.nf], al)) {
+                aligned = aligned && al;
+                ++b.nf;
+            }
+        }
+        if (b.nf > 0) {
+            DevGuard g(h->dev);
+            Prof p(h, IG_K_EXTRAP);
+            CUDA_OK(launch_extrap_batch(b, aligned ? 2 : 1, h->nsm, h->stream));
+            count(h, 1);
+        }
+        i = j;
+    }
+    return IG_OK;
+}
+
+int ig_update_batch(int n, ig_t *hs, const double *const *xs, const double *const *Axs) {
+    if (n < 0 || (n > 0 && (!hs || !xs))) return set_err(IG_E_ARG, "bad batch arguments");
+    for (int i = 0; i < n; ++i) {
+        int rc = ig_update(hs[i], xs[i], Axs ? Axs[i] : nullptr);
+        if (rc) return rc;
+    }
     return IG_OK;
 }
 

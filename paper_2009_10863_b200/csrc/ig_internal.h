@@ -85,6 +85,12 @@ struct ExtrapArgs {
     double *x0;
 };
 
+constexpr int MAXF = 4;  // fields per batched extrapolation launch (u_x, u_y, u_z, p)
+struct ExtrapBatch {
+    ExtrapArgs f[MAXF];
+    int nf;
+};
+
 // ----------------------------------------------------------------------------- launch policy
 // Process-wide launch flags (env IG_LAUNCH, comma list of "coop", "pdl"; default "pdl"):
 //   coop: persistent fused kernels use cooperative launch (co-residency guaranteed by the driver).
@@ -141,6 +147,7 @@ cudaError_t launch_u3(const ProjArgs &a, int vec, int nsm, cudaStream_t s);
 cudaError_t launch_form_fused(const ProjArgs &a, int vec, int nsm, cudaStream_t s);
 cudaError_t launch_update_fused(const ProjArgs &a, int vec, int nsm, cudaStream_t s);
 cudaError_t launch_extrap(const ExtrapArgs &a, int vec, int nsm, cudaStream_t s);
+cudaError_t launch_extrap_batch(const ExtrapBatch &b, int vec, int nsm, cudaStream_t s);
 cudaError_t launch_copy(double *dst, const double *src, int64_t N, int vec, int nsm, cudaStream_t s);
 
 // Cached cudaOccupancyMaxActiveBlocksPerMultiprocessor(kernel, THREADS) (api.cpp); the query is

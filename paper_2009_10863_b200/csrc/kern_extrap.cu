@@ -13,11 +13,10 @@
 namespace ig {
 
 template <int FC, int VEC, int UNROLL>
-__global__ void __launch_bounds__(THREADS, 1) k_extrap(const __grid_constant__ ExtrapArgs a) {
+__device__ __forceinline__ void extrap_body(const ExtrapArgs &a) {
     // All loads of a trip are issued before the FMAs consume them (see kern_proj.cu); the
     // accumulation order is oldest -> newest, like Eq. EXTRAPEXPN.
     typedef typename std::conditional<VEC == 2, double2, double>::type V;
-    pdl_wait();
     // (an L2 evict_first hint on these single-use loads measured 8% SLOWER at N = 2^27: not used)
     const int f = a.f;
     const int64_t nv = a.N / VEC;
@@ -58,6 +57,21 @@ __global__ void __launch_bounds__(THREADS, 1) k_extrap(const __grid_constant__ E
             if (j < f) acc = fma(a.beta[j], a.src[j][e], acc);
         a.x0[e] = acc;
     }
+}
+
+template <int FC, int VEC, int UNROLL>
+__global__ void __launch_bounds__(THREADS, 1) k_extrap(const __grid_constant__ ExtrapArgs a) {
+    pdl_wait();
+    extrap_body<FC, VEC, UNROLL>(a);
+    pdl_trigger();
+}
+
+// Multi-field batch (one history space per field): blockIdx.y
+// selects the field, so the guesses of up to MAXF fields cost one launch.
+template <int FC, int VEC, int UNROLL>
+__global__ void __launch_bounds__(THREADS, 1) k_extrap_batch(const __grid_constant__ ExtrapBatch b) {
+    pdl_wait();
+    extrap_body<FC, VEC, UNROLL>(b.f[blockIdx.y]);
     pdl_trigger();
 }
 
@@ -107,6 +121,42 @@ cudaError_t launch_extrap(const ExtrapArgs &a, int vec, int nsm, cudaStream_t s)
     else if (f <= 8) launch_fc<8>(a, vec, nsm, s);
     else if (f <= 16) launch_fc<16>(a, vec, nsm, s);
     else launch_fc<32>(a, vec, nsm, s);
+    return cudaGetLastError();
+}
+
+template <int FC>
+static void launch_fc_batch(const ExtrapBatch &b, int vec, int nsm, cudaStream_t s) {
+    int64_t nmax = 0;
+    for (int j = 0; j < b.nf; ++j) nmax = b.f[j].N > nmax ? b.f[j].N : nmax;
+    constexpr int U = FC <= 2 ? 4 : (FC <= 4 ? 2 : 1);
+    const LaunchFlags fl = launch_flags();
+    auto go = [&](auto kern, int64_t nv) {
+        cudaLaunchConfig_t cfg = {};
+        int gx = grid_for_x(kern, nv, nsm);
+        gx = (gx + b.nf - 1) / b.nf;  // the fields share the SMs
+        cfg.gridDim = dim3(gx < 1 ? 1 : gx, b.nf);
+        cfg.blockDim = dim3(THREADS);
+        cfg.stream = s;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[0].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = fl.pdl ? 1 : 0;
+        cudaLaunchKernelEx(&cfg, kern, b);
+    };
+    if (vec == 2) go(k_extrap_batch<FC, 2, U>, nmax / 2);
+    else go(k_extrap_batch<FC, 1, U>, nmax);
+}
+
+cudaError_t launch_extrap_batch(const ExtrapBatch &b, int vec, int nsm, cudaStream_t s) {
+    int f = 0;
+    for (int j = 0; j < b.nf; ++j) f = b.f[j].f > f ? b.f[j].f : f;
+    if (f <= 1) launch_fc_batch<1>(b, vec, nsm, s);
+    else if (f <= 2) launch_fc_batch<2>(b, vec, nsm, s);
+    else if (f <= 4) launch_fc_batch<4>(b, vec, nsm, s);
+    else if (f <= 8) launch_fc_batch<8>(b, vec, nsm, s);
+    else if (f <= 16) launch_fc_batch<16>(b, vec, nsm, s);
+    else launch_fc_batch<32>(b, vec, nsm, s);
     return cudaGetLastError();
 }
 

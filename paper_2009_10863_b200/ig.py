@@ -116,6 +116,27 @@ def ig_update(h, x, Ax=None) -> None:
     _check(lib().ig_update(h, _dptr(x, "x"), _dptr(Ax, "Ax")), "ig_update")
 
 
+def _ptr_array(vals):
+    return (C.c_void_p * len(vals))(*[C.c_void_p(v) if v else None for v in vals])
+
+
+def ig_form_guess_batch(handles, bs, x0s) -> None:
+    """Guesses of several fields; consecutive extrapolation fields share one kernel launch."""
+    n = len(handles)
+    hb = _ptr_array([h.h if isinstance(h, InitialGuess) else h for h in handles])
+    bp = _ptr_array([_dptr(b, "b") for b in bs]) if bs is not None else None
+    xp = _ptr_array([_dptr(x, "x0") for x in x0s])
+    _check(lib().ig_form_guess_batch(n, hb, bp, xp), "ig_form_guess_batch")
+
+
+def ig_update_batch(handles, xs, Axs=None) -> None:
+    n = len(handles)
+    hb = _ptr_array([h.h if isinstance(h, InitialGuess) else h for h in handles])
+    xp = _ptr_array([_dptr(x, "x") for x in xs])
+    ap = _ptr_array([_dptr(a, "Ax") for a in Axs]) if Axs is not None else None
+    _check(lib().ig_update_batch(n, hb, xp, ap), "ig_update_batch")
+
+
 def ig_form_guess_host(h, b, x0) -> None:
     _check(lib().ig_form_guess_host(h, _hptr(b, "b"), _hptr(x0, "x0")), "ig_form_guess_host")
 

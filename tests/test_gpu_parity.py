@@ -408,3 +408,36 @@ def test_history_in_caller_storage():
     he.close()
     with pytest.raises(Exception):
         InitialGuess(g.N, "proj_qr", M, storage=sp[:100])  # too small -> IG_E_ARG
+
+
+# ------------------------------------------------------------------ multi-field batch (row f4)
+def test_multi_field_batch_one_launch_for_the_velocity_fields():
+    """u_x, u_y, u_z by EXTRAP (different schemes) and p by QR, as the paper's solver keeps one
+    history space per field (Table 7): one batched call, the three
+    extrapolation guesses share one kernel launch, every guess matches its oracle."""
+    from oracle import ExtrapSparse
+    from paper_2009_10863_b200 import InitialGuess, ig_form_guess_batch, ig_total_launches, ig_update_batch
+
+    g = Grid(30, 2)
+    N = g.N
+    specs = [("extrap_ls", 8, 3), ("extrap_ls", 4, 2), ("extrap_sparse", 8, 2), ("proj_qr", 6, 0)]
+    oras = [ExtrapLS(N, 8, 3), ExtrapLS(N, 4, 2), ExtrapSparse(N, 8, 2), ProjQR(N, 6)]
+    igs = [InitialGuess(N, m, M, p) for m, M, p in specs]
+    seqs = [_seq(g, 14, dt=dt) for dt in (1e-2, 2e-2, 3e-2, 1e-2)]
+    for n in range(14):
+        bs = [torch.from_numpy(s[n][0]).cuda() for s in seqs]
+        x0s = [torch.zeros(N, dtype=torch.float64, device="cuda") for _ in specs]
+        l0 = ig_total_launches()
+        ig_form_guess_batch(igs, bs, x0s)
+        torch.cuda.synchronize()
+        if n >= 8:
+            assert ig_total_launches() - l0 == 2  # one batched extrapolation launch + one QR launch
+        for o, s, x0 in zip(oras, seqs, x0s):
+            assert _rel(x0.cpu().numpy(), o.form_guess(s[n][0], np.zeros(N))) <= TOL, n
+        xs = [torch.from_numpy(s[n][1]).cuda() for s in seqs]
+        As = [torch.from_numpy(s[n][2]).cuda() for s in seqs]
+        ig_update_batch(igs, xs, As)
+        for o, s in zip(oras, seqs):
+            o.update(s[n][1], s[n][2])
+    for ig in igs:
+        ig.close()
