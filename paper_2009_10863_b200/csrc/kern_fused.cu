@@ -291,9 +291,10 @@ __global__ void __launch_bounds__(THREADS, 1) k_update_fused(ProjArgs a) {
     // Serpentine order: pass 2 walks the vectors BACKWARDS, so it starts on the B~/Ax lines pass 1
     // touched last (still in the 126 MB L2); pass 3 walks forwards again and starts on what pass 2
     // touched last.  Same arithmetic per element, fewer HBM bytes per step.
-    const int64_t ntrip2 = (i_first < nv) ? (nv - i_first + U * stride - 1) / (U * stride) : 0;
-    U2Trip<MC, U, V> pre2;
-    if (deff > 0 && ntrip2 > 0) u2trip_load(pre2, a, i_first + (ntrip2 - 1) * U * stride, stride, nv, deff, pol.keep);
+    constexpr int UB = FusedUnroll<MC>::U2;
+    const int64_t ntrip2 = (i_first < nv) ? (nv - i_first + UB * stride - 1) / (UB * stride) : 0;
+    U2Trip<MC, UB, V> pre2;
+    if (deff > 0 && ntrip2 > 0) u2trip_load(pre2, a, i_first + (ntrip2 - 1) * UB * stride, stride, nv, deff, pol.keep);
     block_partials_store<MC + 1>(v, deff, true, a.blk, sh);
     grid_barrier(&c->bar, 1, &c->err, a.watchdog_ns);
     reduce_all_blocks<MC>(deff, true, a.blk, s_r1);
@@ -310,8 +311,8 @@ __global__ void __launch_bounds__(THREADS, 1) k_update_fused(ProjArgs a) {
         for (int k = 0; k <= MC; ++k) v[k] = 0.0;
         if (ntrip2 > 0) u2trip_compute(pre2, c1, v);
         for (int64_t t = ntrip2 - 2; t >= 0; --t) {
-            U2Trip<MC, U, V> r;
-            u2trip_load(r, a, i_first + t * U * stride, stride, nv, deff, pol.keep);
+            U2Trip<MC, UB, V> r;
+            u2trip_load(r, a, i_first + t * UB * stride, stride, nv, deff, pol.keep);
             u2trip_compute(r, c1, v);
         }
         if (tail) {

@@ -483,10 +483,14 @@ __device__ __forceinline__ void u2_trip(const ProjArgs &a, int64_t i0, int64_t s
     }
 }
 
+#ifndef IG_U2_MC8
+#define IG_U2_MC8 2
+#endif
 // Unroll of the fused kernels' d+1-stream passes (registers are sized by the X~ pass anyway).
 template <int MC> struct FusedUnroll {
     static constexpr int U = MC <= 4 ? 4 : (MC <= 8 ? 2 : 1);
     static constexpr int U3 = MC <= 2 ? 4 : (MC <= 4 ? 2 : 1);  // X~ pass (2d+2 streams)
+    static constexpr int U2 = MC <= 4 ? 4 : (MC <= 8 ? IG_U2_MC8 : 1);  // pass 2 (mostly L2 hits)
     // For MC >= 16 the per-column coefficients (c1, c2, Givens c/s) are read from shared memory
     // at each use instead of living in 4*MC registers, which the column loads need.
     static constexpr bool SMEM_COEF = MC >= 16;
