@@ -1,0 +1,135 @@
+"""GPU-side API behaviour: byte accounting, reset, launch policies, per-kernel profiling, errors."""
+
+import os
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import ExtrapLS, ProjQR
+from workloads import Grid, manufactured_step
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _lib():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+
+
+def _seq(g, steps, dt=1e-2):
+    return [tuple(t.numpy() for t in manufactured_step(g, n, dt=dt)) for n in range(steps)]
+
+
+def test_byte_accounting_follows_the_fused_schedule():
+    """ig_bytes = DESIGN.md §7: form 2(d+1); update U1 (2M | d+1) + U2 (d+1) + U3; 8 bytes/value."""
+    from paper_2009_10863_b200 import InitialGuess
+
+    g = Grid(20, 2)
+    N, M = g.N, 5
+    ig = InitialGuess(N, "proj_qr", M)
+    vb = 8 * N
+    d_before = 0
+    for n, (b, x, Ax) in enumerate(_seq(g, 2 * M + 3)):
+        x0 = torch.zeros(N, dtype=torch.float64, device="cuda")
+        ig.form_guess(torch.from_numpy(b).cuda(), x0)
+        fb, _ = ig.bytes()
+        assert fb == (2 * (d_before + 1) * vb if d_before > 0 else 0)
+        ig.update(torch.from_numpy(x).cuda(), torch.from_numpy(Ax).cuda())
+        _, ub = ig.bytes()
+        rot = d_before == M
+        de = M - 1 if rot else d_before
+        expect = (2 * M if rot else de + 1) + (de + 1 if de > 0 else 0) + (1 + de + 1 + 2) + (2 * M - 1 if rot else de)
+        assert ub == expect * vb, (n, ub / vb, expect)
+        d_before = ig.d
+    # steady state: (8M+4) values per element per step
+    assert fb + ub == (8 * M + 4) * vb
+    ig.close()
+
+
+def test_reset_forgets_history():
+    from paper_2009_10863_b200 import InitialGuess
+
+    g = Grid(16, 2)
+    seq = _seq(g, 10)
+    ig, ie = InitialGuess(g.N, "proj_qr", 4), InitialGuess(g.N, "extrap_ls", 4, 2)
+    for b, x, Ax in seq[:6]:
+        ig.update(torch.from_numpy(x).cuda(), torch.from_numpy(Ax).cuda())
+        ie.update(torch.from_numpy(x).cuda())
+    ig.reset()
+    ie.reset()
+    assert ig.d == 0 and ie.d == 0
+    op, oe = ProjQR(g.N, 4), ExtrapLS(g.N, 4, 2)
+    for b, x, Ax in seq[6:]:
+        for o, h in ((op, ig), (oe, ie)):
+            x0 = torch.full((g.N,), 2.0, dtype=torch.float64, device="cuda")
+            h.form_guess(torch.from_numpy(b).cuda(), x0)
+            ref = o.form_guess(b, np.full(g.N, 2.0))
+            assert np.linalg.norm(x0.cpu().numpy() - ref) <= 1e-11 * np.linalg.norm(ref)
+            o.update(x, Ax)
+            h.update(torch.from_numpy(x).cuda(), torch.from_numpy(Ax).cuda())
+    ig.close()
+    ie.close()
+
+
+@pytest.mark.parametrize("flags", ["coop,pdl", "coop", "", "pdl"])
+def test_launch_policies_give_identical_results(flags):
+    """IG_LAUNCH selects cooperative launch and/or programmatic dependent launch; the arithmetic
+    (and therefore every bit of the guesses) must not depend on it."""
+    code = (
+        "import numpy as np, torch, sys\n"
+        f"sys.path.insert(0, {ROOT!r})\n"
+        "from paper_2009_10863_b200 import InitialGuess\n"
+        "from workloads import Grid, manufactured_step\n"
+        "g = Grid(64, 2); ig = InitialGuess(g.N, 'proj_qr', 6); ie = InitialGuess(g.N, 'extrap_ls', 6, 2)\n"
+        "out = []\n"
+        "for n in range(14):\n"
+        "    b, x, Ax = (t.cuda() for t in manufactured_step(g, n, dt=1e-2))\n"
+        "    x0 = torch.zeros_like(b); ig.form_guess(b, x0); out.append(x0.cpu().numpy())\n"
+        "    y0 = torch.zeros_like(b); ie.form_guess(None, y0); out.append(y0.cpu().numpy())\n"
+        "    ig.update(x, Ax); ie.update(x)\n"
+        "np.save(sys.argv[1], np.stack(out))\n"
+    )
+    import tempfile
+
+    with tempfile.TemporaryDirectory() as td:
+        res = {}
+        for f in (flags, "pdl"):
+            path = os.path.join(td, f"out_{f or 'none'}.npy")
+            env = dict(os.environ, IG_LAUNCH=f if f else "none")
+            r = subprocess.run([sys.executable, "-c", code, path], env=env, capture_output=True, text=True, timeout=300)
+            assert r.returncode == 0, r.stderr
+            res[f] = np.load(path)
+        assert np.array_equal(res[flags], res["pdl"])  # bitwise identical (same grid, same order)
+
+
+def test_profile_counts_launches():
+    from paper_2009_10863_b200 import InitialGuess, ig_profile, ig_profile_read
+
+    g = Grid(32, 2)
+    ig = InitialGuess(g.N, "proj_qr", 4)
+    ig_profile(ig.h, True)
+    for b, x, Ax in _seq(g, 6):
+        x0 = torch.zeros(g.N, dtype=torch.float64, device="cuda")
+        ig.form_guess(torch.from_numpy(b).cuda(), x0)
+        ig.update(torch.from_numpy(x).cuda(), torch.from_numpy(Ax).cuda())
+    prof = ig_profile_read(ig.h)
+    assert prof["update_fused"][1] == 6 and prof["form_fused"][1] == 6
+    assert prof["update_fused"][0] > 0.0
+    ig_profile(ig.h, False)
+    ig.close()
+
+
+def test_argument_errors_on_device():
+    from paper_2009_10863_b200 import IGError, InitialGuess
+
+    ig = InitialGuess(100, "proj_qr", 4)
+    with pytest.raises(TypeError):
+        ig.form_guess(torch.zeros(100, dtype=torch.float32, device="cuda"), torch.zeros(100, device="cuda"))
+    with pytest.raises(IGError, match="Ax is NULL"):
+        ig.update(torch.zeros(100, dtype=torch.float64, device="cuda"), None)
+    ig.close()
