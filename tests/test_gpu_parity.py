@@ -441,3 +441,28 @@ def test_multi_field_batch_one_launch_for_the_velocity_fields():
             o.update(s[n][1], s[n][2])
     for ig in igs:
         ig.close()
+
+
+@pytest.mark.parametrize("eps", [1e-4, 1e-6, 0.0])
+def test_admission_tolerance_parity(eps):
+    """ig_set_admit_tol (AMB-3): with a tolerance above the sequence's rho ~ 1e-6..1e-5 most pairs
+    are rejected; the CUDA path must take exactly the oracle's decisions."""
+    from paper_2009_10863_b200 import InitialGuess
+
+    g = Grid(32, 2)
+    seq = _seq(g, 20)
+    ora = ProjQR(g.N, 6, eps)
+    ig = InitialGuess(g.N, "proj_qr", 6, eps=eps)
+    ds = []
+    for b, x, Ax in seq:
+        x0 = torch.zeros(g.N, dtype=torch.float64, device="cuda")
+        ig.form_guess(torch.from_numpy(b).cuda(), x0)
+        assert _rel(x0.cpu().numpy(), ora.form_guess(b, np.zeros(g.N))) <= TOL
+        ora.update(x, Ax)
+        ig.update(torch.from_numpy(x).cuda(), torch.from_numpy(Ax).cuda())
+        st = ig.stats()
+        assert (st["d"], bool(st["admitted"])) == (ora.d, ora.admitted)
+        ds.append(ora.d)
+    if eps >= 1e-4:
+        assert max(ds) < 6  # the tolerance really rejected pairs
+    ig.close()
