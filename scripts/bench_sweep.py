@@ -55,6 +55,7 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--mem-gb", type=float, default=150.0)
     ap.add_argument("--out", default=None)
+    ap.add_argument("--degree", type=int, default=None, help="EXTRAP degree (default floor(sqrt(M)), P:1527-1529)")
     a = ap.parse_args()
     P = peak()
     rows = []
@@ -62,7 +63,7 @@ def main():
         for M in [int(x) for x in a.ms.split(",")]:
             vb = 8 * N
             pool = M + 2
-            need = (2 * M + 2 * pool + 4) * vb / 1e9
+            need = (2 * M + 2 * pool + 2) * vb / 1e9
             if need > a.mem_gb:
                 rows.append({"N": N, "M": M, "skipped": f"needs {need:.0f} GB"})
                 continue
@@ -82,7 +83,7 @@ def main():
             assert hp.d == M and hp.stats()["admitted"] == 1
             hp.close()
             del hp
-            p = int(math.isqrt(M)) if M > 1 else 0
+            p = (int(math.isqrt(M)) if M > 1 else 0) if a.degree is None else a.degree
             p = min(p, M - 1)
             he = InitialGuess(N, "extrap_ls", M, p)
 
