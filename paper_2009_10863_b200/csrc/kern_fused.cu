@@ -22,149 +22,6 @@ namespace ig {
 // partials a slow CTA is still reading.
 constexpr int BLK2 = PS * MAXB;
 
-// ------------------------------------------------------------------ trip = loads, then arithmetic
-// The first trip of the pass AFTER a grid barrier is loaded BEFORE the barrier (the addresses do
-// not depend on the reduction; each thread only reads rows it wrote itself in earlier passes), so
-// the barrier + all-CTA reduction bubble overlaps useful HBM traffic.
-
-template <int MC, int U, class V> struct XTrip {  // form pass 2: U strided elements of d X~ columns
-    V col[U][MC];
-};
-template <int MC, int U, class V>
-__device__ __forceinline__ void xtrip_load(XTrip<MC, U, V> &r, const ProjArgs &a, int64_t i0, int64_t stride,
-                                           int64_t nv, int d, unsigned long long ps) {
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-        const int64_t i = i0 + u * stride;
-#pragma unroll
-        for (int k = 0; k < MC; ++k) r.col[u][k] = (i < nv && k < d) ? ldp<V>(a.Xt + k * a.ld, i, ps) : vzero(V());
-    }
-}
-template <int MC, int U, class V>
-__device__ __forceinline__ void xtrip_store(const XTrip<MC, U, V> &r, const ProjArgs &a, int64_t i0, int64_t stride,
-                                            int64_t nv, const double *al) {
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-        const int64_t i = i0 + u * stride;
-        V acc = vzero(V());
-#pragma unroll
-        for (int k = 0; k < MC; ++k) acc = vaxpy(al[k], r.col[u][k], acc);
-        if (i < nv) stv<V>(a.x0, i, acc);
-    }
-}
-
-template <int MC, int U, class V> struct U2Trip {  // update pass 2
-    V ax[U];
-    V col[U][MC];
-};
-template <int MC, int U, class V>
-__device__ __forceinline__ void u2trip_load(U2Trip<MC, U, V> &r, const ProjArgs &a, int64_t i0, int64_t stride,
-                                            int64_t nv, int deff, unsigned long long pk) {
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-        const int64_t i = i0 + u * stride;
-        const bool ok = i < nv;
-        r.ax[u] = ok ? ldp<V>(a.Ax, i, pk) : vzero(V());
-#pragma unroll
-        for (int k = 0; k < MC; ++k) r.col[u][k] = (ok && k < deff) ? ldp<V>(a.Bt + k * a.ld, i, pk) : vzero(V());
-    }
-}
-template <int MC, int U, class V, class CP>
-__device__ __forceinline__ void u2trip_compute(const U2Trip<MC, U, V> &r, CP c1, double (&v)[MC + 1]) {
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-        V b1 = r.ax[u];  // b1 = Ax - B~ c1 (registers only)
-#pragma unroll
-        for (int k = 0; k < MC; ++k) b1 = vaxpy(-c1[k], r.col[u][k], b1);
-#pragma unroll
-        for (int k = 0; k < MC; ++k) v[k] = vdot(r.col[u][k], b1, v[k]);
-        v[MC] = vdot(b1, b1, v[MC]);
-    }
-}
-
-// For MC >= 32 (SPLIT) a trip holds only Ax, x and the B~ columns; the X~ columns are loaded
-// (all at once) after the B~ part is finished, so the two 32-column register sets are never live
-// together and the pass can use 16-byte loads (VEC = 2) within the register file.
-template <int MC, int U, class V> struct U3Trip {  // update pass 3: U strided elements
-    static constexpr bool SPLIT = MC >= 32;
-    V ax[U], xv[U];
-    V bc[U][MC];
-    V xc[U][SPLIT ? 1 : MC];
-};
-template <int MC, class V>
-__device__ __forceinline__ void u3_load_x(V (&xc)[MC], const ProjArgs &a, int64_t i, bool ok, int nX,
-                                          unsigned long long ps) {
-#pragma unroll
-    for (int k = 0; k < MC; ++k) xc[k] = (ok && k < nX) ? ldp<V>(a.Xt + k * a.ld, i, ps) : vzero(V());
-}
-// Loads assume the pair is admitted (the common case); if it is not, the prefetched B~/Ax/x
-// values of that one trip are simply unused.
-template <int MC, int U, class V>
-__device__ __forceinline__ void u3trip_load(U3Trip<MC, U, V> &r, const ProjArgs &a, int64_t i0, int64_t stride,
-                                            int64_t nv, int deff, bool rotX, bool adm, unsigned long long ps) {
-    const int nB = adm ? deff : 0;
-    const int nX = rotX ? a.M : nB;
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-        const int64_t i = i0 + u * stride;
-        const bool ok = i < nv;
-        r.ax[u] = (ok && adm) ? ldp<V>(a.Ax, i, ps) : vzero(V());
-        r.xv[u] = (ok && adm) ? ldp<V>(a.x, i, ps) : vzero(V());
-#pragma unroll
-        for (int k = 0; k < MC; ++k) r.bc[u][k] = (ok && k < nB) ? ldp<V>(a.Bt + k * a.ld, i, ps) : vzero(V());
-        if constexpr (!U3Trip<MC, U, V>::SPLIT) u3_load_x<MC, V>(r.xc[u], a, i, ok, nX, ps);
-    }
-}
-template <int MC, class V, class CP>
-__device__ __forceinline__ void u3_x_part(const V (&xc)[MC], const ProjArgs &a, int64_t i, bool rotX, V &xt, V &t2,
-                                          CP c1, CP c2, CP gc, CP gs, unsigned long long ps) {
-    if (rotX) {
-        V t = xc[0];
-#pragma unroll
-        for (int k = 0; k < MC - 1; ++k) {
-            if (k < a.M - 1) {
-                V nk;
-                vrot(gc[k], gs[k], t, xc[k + 1], nk);
-                stp<V>(a.Xt + k * a.ld, i, nk, ps);
-                xt = vaxpy(-c1[k], nk, xt);
-                t2 = vaxpy(c2[k], nk, t2);
-            }
-        }
-    } else {
-#pragma unroll
-        for (int k = 0; k < MC; ++k) {
-            xt = vaxpy(-c1[k], xc[k], xt);
-            t2 = vaxpy(c2[k], xc[k], t2);
-        }
-    }
-}
-template <int MC, int U, class V, class CP>
-__device__ __forceinline__ void u3trip_store(const U3Trip<MC, U, V> &r, const ProjArgs &a, int64_t i0,
-                                             int64_t stride, int64_t nv, int deff, bool rotX, bool adm, double inv,
-                                             CP c1, CP c2, CP gc, CP gs, unsigned long long ps) {
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-        const int64_t i = i0 + u * stride;
-        if (i >= nv) break;
-        // b~ = (Ax - B~ c1) - B~ c2 ; x~ = (x - X~ c1) - X~ c2 (separate corrections, DESIGN.md AMB-7)
-        V b1 = r.ax[u], s2 = vzero(V());
-#pragma unroll
-        for (int k = 0; k < MC; ++k) b1 = vaxpy(-c1[k], r.bc[u][k], b1);
-#pragma unroll
-        for (int k = 0; k < MC; ++k) s2 = vaxpy(c2[k], r.bc[u][k], s2);
-        if (adm) stp<V>(a.Bt + deff * a.ld, i, vscale(inv, vaxpy(-1.0, s2, b1)), ps);
-        V xt = r.xv[u], t2 = vzero(V());
-        if constexpr (U3Trip<MC, U, V>::SPLIT) {
-            V xc[MC];
-            u3_load_x<MC, V>(xc, a, i, true, rotX ? a.M : (adm ? deff : 0), ps);
-            u3_x_part<MC, V>(xc, a, i, rotX, xt, t2, c1, c2, gc, gs, ps);
-        } else {
-            u3_x_part<MC, V>(r.xc[u], a, i, rotX, xt, t2, c1, c2, gc, gs, ps);
-        }
-        if (adm) stp<V>(a.Xt + deff * a.ld, i, vscale(inv, vaxpy(-1.0, t2, xt)), ps);
-    }
-}
-
 template <int MC, int VEC>
 __global__ void __launch_bounds__(THREADS, 1) k_form_fused(ProjArgs a) {
     typedef typename VT<VEC>::T V;

@@ -106,9 +106,13 @@ __global__ void __launch_bounds__(THREADS, 1) k_form_combine(ProjArgs a) {
 }
 
 // ------------------------------------------------------------------ update pass 1 (+ B~ downdate)
+// The three update kernels use the same trip functions (proj_common.cuh) as the persistent
+// k_update_fused; here each pass is its own launch so the per-rank partials can be all-gathered
+// with NCCL in between (multi-rank schedule without peer windows).
 template <int MC, int VEC>
 __global__ void __launch_bounds__(THREADS, 1) k_u1(ProjArgs a) {
     typedef typename VT<VEC>::T V;
+    constexpr int U = FusedUnroll<MC>::U;
     pdl_wait();
     __shared__ double sh[(THREADS / 32) * (MC + 1)];
     __shared__ double s_gc[MAXM], s_gs[MAXM];
@@ -117,26 +121,25 @@ __global__ void __launch_bounds__(THREADS, 1) k_u1(ProjArgs a) {
     const bool pend = c->pending != 0;
     const bool restart = (a.method == M_PROJ_CLASSIC) && (d >= M);  // Alg. 1 restart
     const int deff = pend ? M - 1 : (restart ? 0 : d);
-    if (pend && threadIdx.x < M - 1) {
-        s_gc[threadIdx.x] = c->gc[threadIdx.x];
-        s_gs[threadIdx.x] = c->gs[threadIdx.x];
+    if (threadIdx.x < MAXM) {
+        const bool rot = pend && threadIdx.x < M - 1;
+        s_gc[threadIdx.x] = rot ? c->gc[threadIdx.x] : 1.0;
+        s_gs[threadIdx.x] = rot ? c->gs[threadIdx.x] : 0.0;
     }
     __syncthreads();
-    double gc[MC], gs[MC];
-#pragma unroll
-    for (int k = 0; k < MC; ++k) {
-        gc[k] = (pend && k < M - 1) ? s_gc[k] : 1.0;
-        gs[k] = (pend && k < M - 1) ? s_gs[k] : 0.0;
-    }
+    Coef<MC> cgc, cgs;
+    const auto gc = cgc.bind(s_gc);
+    const auto gs = cgs.bind(s_gs);
+    const L2Pol pol = make_l2pol();
     double v[MC + 1];
 #pragma unroll
     for (int k = 0; k <= MC; ++k) v[k] = 0.0;
     const int64_t nv = a.N / VEC;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nv; i += stride)
-        u1_elem<MC, V>(a, i, pend, deff, gc, gs, v);
+    for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i0 < nv; i0 += U * stride)
+        u1_trip<MC, U, V>(a, i0, stride, nv, pend, deff, gc, gs, v, pol.keep);
     if (VEC == 2 && (a.N & 1) && blockIdx.x == 0 && threadIdx.x == 0)
-        u1_elem<MC, double>(a, a.N - 1, pend, deff, gc, gs, v);
+        u1_trip<MC, 1, double>(a, a.N - 1, 1, a.N, pend, deff, gc, gs, v, pol.keep);
     if (block_partials_ticket<MC + 1>(v, deff, true, a.blk, &c->ticket[ST_U1], sh)) {
         final_reduce<MC>(deff, true, a.blk, a.part + ST_U1 * PS);
         if (pend)
@@ -149,72 +152,53 @@ __global__ void __launch_bounds__(THREADS, 1) k_u1(ProjArgs a) {
             c->ticket[ST_U1] = 0;
         }
     }
+    pdl_trigger();
 }
 
 // ------------------------------------------------------------------ update pass 2
 template <int MC, int VEC>
 __global__ void __launch_bounds__(THREADS, 1) k_u2(ProjArgs a) {
     typedef typename VT<VEC>::T V;
+    constexpr int U = FusedUnroll<MC>::U2;
     pdl_wait();
-    constexpr int U = Unroll<MC>::U;
     __shared__ double sh[(THREADS / 32) * (MC + 1)];
     __shared__ double s_c1[MAXM];
     Ctrl *c = a.ctrl;
     const int deff = c->deff;
     if (deff == 0) return;  // d = 0 path: nothing to orthogonalise against
     const double *g1 = a.gath + ST_U1 * a.G * PS;
-    if (threadIdx.x < deff) s_c1[threadIdx.x] = rank_sum(g1, a.G, threadIdx.x);
+    if (threadIdx.x < MAXM) s_c1[threadIdx.x] = (threadIdx.x < deff) ? rank_sum(g1, a.G, threadIdx.x) : 0.0;
     __syncthreads();
-    double c1[MC];
-#pragma unroll
-    for (int k = 0; k < MC; ++k) c1[k] = (k < deff) ? s_c1[k] : 0.0;
+    Coef<MC> cc1;
+    const auto c1 = cc1.bind(s_c1);
+    const L2Pol pol = make_l2pol();
     double v[MC + 1];
 #pragma unroll
     for (int k = 0; k <= MC; ++k) v[k] = 0.0;
     const int64_t nv = a.N / VEC;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i0 < nv; i0 += U * stride) {
-        V ax[U], col[U][MC];
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-            const int64_t i = i0 + u * stride;
-            const bool ok = i < nv;
-            ax[u] = ok ? ldro<V>(a.Ax, i) : vzero(V());
-#pragma unroll
-            for (int k = 0; k < MC; ++k) col[u][k] = (ok && k < deff) ? ldro<V>(a.Bt + k * a.ld, i) : vzero(V());
-        }
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-            V b1 = ax[u];  // b1 = Ax - B~ c1, formed in registers only
-#pragma unroll
-            for (int k = 0; k < MC; ++k) b1 = vaxpy(-c1[k], col[u][k], b1);
-#pragma unroll
-            for (int k = 0; k < MC; ++k) v[k] = vdot(col[u][k], b1, v[k]);
-            v[MC] = vdot(b1, b1, v[MC]);
-        }
+        U2Trip<MC, U, V> r;
+        u2trip_load(r, a, i0, stride, nv, deff, pol.keep);
+        u2trip_compute(r, c1, v);
     }
     if (VEC == 2 && (a.N & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
-        const int64_t i = a.N - 1;
-        double col[MC];
-#pragma unroll
-        for (int k = 0; k < MC; ++k) col[k] = (k < deff) ? a.Bt[k * a.ld + i] : 0.0;
-        double b1 = a.Ax[i];
-#pragma unroll
-        for (int k = 0; k < MC; ++k) b1 = fma(-c1[k], col[k], b1);
-#pragma unroll
-        for (int k = 0; k < MC; ++k) v[k] = fma(col[k], b1, v[k]);
-        v[MC] = fma(b1, b1, v[MC]);
+        U2Trip<MC, 1, double> r;
+        u2trip_load(r, a, a.N - 1, 1, a.N, deff, pol.keep);
+        u2trip_compute(r, c1, v);
     }
     if (block_partials_ticket<MC + 1>(v, deff, true, a.blk, &c->ticket[ST_U2], sh)) {
         final_reduce<MC>(deff, true, a.blk, a.part + ST_U2 * PS);
         if (threadIdx.x == 0) c->ticket[ST_U2] = 0;
     }
+    pdl_trigger();
 }
 
 // ------------------------------------------------------------------ update store (+ X~ downdate)
 template <int MC, int VEC>
 __global__ void __launch_bounds__(THREADS, 1) k_u3(ProjArgs a) {
     typedef typename VT<VEC>::T V;
+    constexpr int U3 = FusedUnroll<MC>::U3;
     pdl_wait();
     __shared__ double s_c1[MAXM], s_c2[MAXM], s_gc[MAXM], s_gs[MAXM];
     __shared__ double s_nb, s_nAx;
@@ -226,13 +210,13 @@ __global__ void __launch_bounds__(THREADS, 1) k_u3(ProjArgs a) {
     const bool rotX = c->rotX != 0;
     const double *g1 = a.gath + ST_U1 * a.G * PS;
     const double *g2 = a.gath + ST_U2 * a.G * PS;
-    if (threadIdx.x < deff) {
-        s_c1[threadIdx.x] = rank_sum(g1, a.G, threadIdx.x);
-        s_c2[threadIdx.x] = rank_sum(g2, a.G, threadIdx.x);
-    }
-    if (rotX && threadIdx.x < M - 1) {
-        s_gc[threadIdx.x] = c->gc[threadIdx.x];
-        s_gs[threadIdx.x] = c->gs[threadIdx.x];
+    if (threadIdx.x < MAXM) {
+        const int t = threadIdx.x;
+        s_c1[t] = (t < deff) ? rank_sum(g1, a.G, t) : 0.0;
+        s_c2[t] = (t < deff) ? rank_sum(g2, a.G, t) : 0.0;
+        const bool rot = rotX && t < M - 1;
+        s_gc[t] = rot ? c->gc[t] : 1.0;
+        s_gs[t] = rot ? c->gs[t] : 0.0;
     }
     if (threadIdx.x == 0) {
         const double nAx2 = rank_sum(g1, a.G, NORM);
@@ -255,22 +239,27 @@ __global__ void __launch_bounds__(THREADS, 1) k_u3(ProjArgs a) {
     __syncthreads();
     const bool adm = s_adm != 0;
     const double inv = adm ? 1.0 / s_nb : 0.0;
-    double c1[MC], c2[MC], gc[MC], gs[MC];
-#pragma unroll
-    for (int k = 0; k < MC; ++k) {
-        c1[k] = (k < deff) ? s_c1[k] : 0.0;
-        c2[k] = (k < deff) ? s_c2[k] : 0.0;
-        gc[k] = (rotX && k < M - 1) ? s_gc[k] : 1.0;
-        gs[k] = (rotX && k < M - 1) ? s_gs[k] : 0.0;
-    }
+    Coef<MC> cc1, cc2, cgc, cgs;
+    const auto c1 = cc1.bind(s_c1);
+    const auto c2 = cc2.bind(s_c2);
+    const auto gc = cgc.bind(s_gc);
+    const auto gs = cgs.bind(s_gs);
+    const L2Pol pol = make_l2pol();
     if (adm || rotX) {
         const int64_t nv = a.N / VEC;
         const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-        for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nv; i += stride)
-            u3_elem<MC, V>(a, i, deff, rotX, adm, inv, c1, c2, gc, gs);
-        if (VEC == 2 && (a.N & 1) && blockIdx.x == 0 && threadIdx.x == 0)
-            u3_elem<MC, double>(a, a.N - 1, deff, rotX, adm, inv, c1, c2, gc, gs);
+        for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i0 < nv; i0 += U3 * stride) {
+            U3Trip<MC, U3, V> r;
+            u3trip_load(r, a, i0, stride, nv, deff, rotX, adm, pol.stream);
+            u3trip_store(r, a, i0, stride, nv, deff, rotX, adm, inv, c1, c2, gc, gs, pol.stream);
+        }
+        if (VEC == 2 && (a.N & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
+            U3Trip<MC, 1, double> r;
+            u3trip_load(r, a, a.N - 1, 1, a.N, deff, rotX, adm, pol.stream);
+            u3trip_store(r, a, a.N - 1, 1, a.N, deff, rotX, adm, inv, c1, c2, gc, gs, pol.stream);
+        }
     }
+    pdl_trigger();
     __threadfence();
     __syncthreads();
     if (threadIdx.x == 0) s_ticket = atomicAdd(&c->ticket[ST_U3], 1u);
@@ -314,7 +303,7 @@ static int mc_bucket(int M) { return M <= 1 ? 1 : M <= 2 ? 2 : M <= 4 ? 4 : M <=
 #define IG_DISPATCH(KERNEL, ARGS, VEC_IN, NSM, STREAM)                                                      \
     do {                                                                                                    \
         const int mc = mc_bucket((ARGS).M);                                                                 \
-        const bool v2 = ((VEC_IN) == 2) && mc <= 8;                                                         \
+        const bool v2 = ((VEC_IN) == 2);                                                                    \
         const int64_t nv = (ARGS).N / (v2 ? 2 : 1);                                                         \
         switch (mc) {                                                                                       \
         case 1: if (v2) { auto k = KERNEL<1, 2>; launch_ex(k, grid_for(k, nv, NSM), STREAM, false, ARGS); }    \
@@ -325,8 +314,10 @@ static int mc_bucket(int M) { return M <= 1 ? 1 : M <= 2 ? 2 : M <= 4 ? 4 : M <=
                 else { auto k = KERNEL<4, 1>; launch_ex(k, grid_for(k, nv, NSM), STREAM, false, ARGS); } break; \
         case 8: if (v2) { auto k = KERNEL<8, 2>; launch_ex(k, grid_for(k, nv, NSM), STREAM, false, ARGS); }    \
                 else { auto k = KERNEL<8, 1>; launch_ex(k, grid_for(k, nv, NSM), STREAM, false, ARGS); } break; \
-        case 16: { auto k = KERNEL<16, 1>; launch_ex(k, grid_for(k, nv, NSM), STREAM, false, ARGS); } break;  \
-        default: { auto k = KERNEL<32, 1>; launch_ex(k, grid_for(k, nv, NSM), STREAM, false, ARGS); } break;  \
+        case 16: if (v2) { auto k = KERNEL<16, 2>; launch_ex(k, grid_for(k, nv, NSM), STREAM, false, ARGS); }  \
+                 else { auto k = KERNEL<16, 1>; launch_ex(k, grid_for(k, nv, NSM), STREAM, false, ARGS); } break; \
+        default: if (v2) { auto k = KERNEL<32, 2>; launch_ex(k, grid_for(k, nv, NSM), STREAM, false, ARGS); }  \
+                 else { auto k = KERNEL<32, 1>; launch_ex(k, grid_for(k, nv, NSM), STREAM, false, ARGS); } break; \
         }                                                                                                   \
     } while (0)
 

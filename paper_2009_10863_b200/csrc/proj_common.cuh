@@ -1,6 +1,8 @@
 // proj_common.cuh -- device helpers shared by the projection kernels (kern_proj.cu: one kernel per
 // pass, used with G > 1 ranks; kern_fused.cu: persistent fused kernels, single GPU).
 #pragma once
+#include <type_traits>
+
 #include "ig_internal.h"
 
 namespace ig {
@@ -328,103 +330,6 @@ template <int MC> struct Unroll {
     static constexpr int U = MC <= 2 ? 4 : (MC <= 4 ? 2 : 1);
 };
 
-template <int MC, class V>
-__device__ __forceinline__ void u2_elem(const ProjArgs &a, int64_t i, int deff, const double *c1,
-                                        double (&v)[MC + 1]) {
-    V col[MC];
-    const V ax = ldro<V>(a.Ax, i);
-#pragma unroll
-    for (int k = 0; k < MC; ++k) col[k] = (k < deff) ? ldro<V>(a.Bt + k * a.ld, i) : vzero(V());
-    V b1 = ax;  // b1 = Ax - B~ c1, formed in registers only
-#pragma unroll
-    for (int k = 0; k < MC; ++k) b1 = vaxpy(-c1[k], col[k], b1);
-#pragma unroll
-    for (int k = 0; k < MC; ++k) v[k] = vdot(col[k], b1, v[k]);
-    v[MC] = vdot(b1, b1, v[MC]);
-}
-
-template <int MC, class V>
-__device__ __forceinline__ void u1_elem(const ProjArgs &a, int64_t i, bool pend, int deff, const double *gc,
-                                        const double *gs, double (&v)[MC + 1]) {
-    const int nload = pend ? a.M : deff;
-    V col[MC];
-    const V ax = ldro<V>(a.Ax, i);
-#pragma unroll
-    for (int k = 0; k < MC; ++k) col[k] = (k < nload) ? ldrw<V>(a.Bt + k * a.ld, i) : vzero(V());
-    v[MC] = vdot(ax, ax, v[MC]);
-    if (pend) {
-        // Givens sweep over B~ column pairs streamed in registers (App. A
-        // P:1800-1815): new column k = c_k t + s_k B_{k+1}; t carries the rotated remainder.
-        V t = col[0];
-#pragma unroll
-        for (int k = 0; k < MC - 1; ++k) {
-            if (k < a.M - 1) {
-                V nk;
-                vrot(gc[k], gs[k], t, col[k + 1], nk);
-                stv<V>(a.Bt + k * a.ld, i, nk);
-                v[k] = vdot(nk, ax, v[k]);
-            }
-        }
-    } else {
-#pragma unroll
-        for (int k = 0; k < MC; ++k) v[k] = vdot(col[k], ax, v[k]);
-    }
-}
-
-template <int MC, class V>
-__device__ __forceinline__ void u3_elem(const ProjArgs &a, int64_t i, int deff, bool rotX, bool adm,
-                                        double inv, const double *c1, const double *c2, const double *gc,
-                                        const double *gs) {
-    // loads first: Ax, x, B~ (admitted), X~ (rotated and/or combined)
-    const int nB = adm ? deff : 0;
-    const int nX = rotX ? a.M : nB;
-    V ax = vzero(V()), xv = vzero(V());
-    V bc[MC], xc[MC];
-    if (adm) {
-        ax = ldro<V>(a.Ax, i);
-        xv = ldro<V>(a.x, i);
-    }
-#pragma unroll
-    for (int k = 0; k < MC; ++k) bc[k] = (k < nB) ? ldro<V>(a.Bt + k * a.ld, i) : vzero(V());
-#pragma unroll
-    for (int k = 0; k < MC; ++k) xc[k] = (k < nX) ? ldrw<V>(a.Xt + k * a.ld, i) : vzero(V());
-    // The two Gram-Schmidt corrections are applied SEPARATELY, as in the listing:
-    // b~ = (Ax - B~ c1) - B~ c2, x~ = (x - X~ c1) - X~ c2.  Folding them into c1+c2 first would
-    // round away c2 (|c2| ~ u |c1|) and undo the re-orthogonalisation (AMB-7).
-    V b1 = ax, s2 = vzero(V());
-#pragma unroll
-    for (int k = 0; k < MC; ++k) b1 = vaxpy(-c1[k], bc[k], b1);  // same FMA order as k_u2
-#pragma unroll
-    for (int k = 0; k < MC; ++k) s2 = vaxpy(c2[k], bc[k], s2);
-    V xt = xv, t2 = vzero(V());
-    if (rotX) {
-        V t = xc[0];
-#pragma unroll
-        for (int k = 0; k < MC - 1; ++k) {
-            if (k < a.M - 1) {
-                V nk;
-                vrot(gc[k], gs[k], t, xc[k + 1], nk);
-                stv<V>(a.Xt + k * a.ld, i, nk);
-                xt = vaxpy(-c1[k], nk, xt);
-                t2 = vaxpy(c2[k], nk, t2);
-            }
-        }
-    } else {
-#pragma unroll
-        for (int k = 0; k < MC; ++k) {
-            xt = vaxpy(-c1[k], xc[k], xt);
-            t2 = vaxpy(c2[k], xc[k], t2);
-        }
-    }
-    if (adm) {  // "B~_{d+1} <- b~/||b~||, X~_{d+1} <- x~/||b~||" (rhsUpdateSpace)
-        stv<V>(a.Bt + deff * a.ld, i, vscale(inv, vaxpy(-1.0, s2, b1)));
-        stv<V>(a.Xt + deff * a.ld, i, vscale(inv, vaxpy(-1.0, t2, xt)));
-    }
-}
-
-
-// U-way unrolled variants (U strided elements per trip, all loads of the trip first): more bytes
-// in flight per thread for the passes that stream only d+1 vectors.
 template <int MC, int U, class V, class CP>
 __device__ __forceinline__ void u1_trip(const ProjArgs &a, int64_t i0, int64_t stride, int64_t nv, bool pend,
                                         int deff, CP gc, CP gs, double (&v)[MC + 1], unsigned long long pk) {
@@ -486,6 +391,24 @@ __device__ __forceinline__ void u2_trip(const ProjArgs &a, int64_t i0, int64_t s
 #ifndef IG_U2_MC8
 #define IG_U2_MC8 2
 #endif
+// Per-column coefficient access: registers for MC <= 8, shared memory (re-read at each use) for
+// larger buckets.  Fills `reg` from `smem` when registers are used and returns the pointer type
+// the trip functions index.
+template <int MC> struct Coef {
+    static constexpr bool SMEM = MC >= 16;
+    typedef typename std::conditional<SMEM, const volatile double *, const double *>::type P;
+    double reg[SMEM ? 1 : MC];
+    __device__ __forceinline__ P bind(const double *smem) {
+        if constexpr (SMEM) {
+            return (P)smem;
+        } else {
+#pragma unroll
+            for (int k = 0; k < MC; ++k) reg[k] = smem[k];
+            return (P)reg;
+        }
+    }
+};
+
 // Unroll of the fused kernels' d+1-stream passes (registers are sized by the X~ pass anyway).
 template <int MC> struct FusedUnroll {
     static constexpr int U = MC <= 4 ? 4 : (MC <= 8 ? 2 : 1);
@@ -495,6 +418,149 @@ template <int MC> struct FusedUnroll {
     // at each use instead of living in 4*MC registers, which the column loads need.
     static constexpr bool SMEM_COEF = MC >= 16;
 };
+
+// ------------------------------------------------------------------ trip = loads, then arithmetic
+// The first trip of the pass AFTER a grid barrier is loaded BEFORE the barrier (the addresses do
+// not depend on the reduction; each thread only reads rows it wrote itself in earlier passes), so
+// the barrier + all-CTA reduction bubble overlaps useful HBM traffic.
+
+template <int MC, int U, class V> struct XTrip {  // form pass 2: U strided elements of d X~ columns
+    V col[U][MC];
+};
+template <int MC, int U, class V>
+__device__ __forceinline__ void xtrip_load(XTrip<MC, U, V> &r, const ProjArgs &a, int64_t i0, int64_t stride,
+                                           int64_t nv, int d, unsigned long long ps) {
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+        const int64_t i = i0 + u * stride;
+#pragma unroll
+        for (int k = 0; k < MC; ++k) r.col[u][k] = (i < nv && k < d) ? ldp<V>(a.Xt + k * a.ld, i, ps) : vzero(V());
+    }
+}
+template <int MC, int U, class V>
+__device__ __forceinline__ void xtrip_store(const XTrip<MC, U, V> &r, const ProjArgs &a, int64_t i0, int64_t stride,
+                                            int64_t nv, const double *al) {
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+        const int64_t i = i0 + u * stride;
+        V acc = vzero(V());
+#pragma unroll
+        for (int k = 0; k < MC; ++k) acc = vaxpy(al[k], r.col[u][k], acc);
+        if (i < nv) stv<V>(a.x0, i, acc);
+    }
+}
+
+template <int MC, int U, class V> struct U2Trip {  // update pass 2
+    V ax[U];
+    V col[U][MC];
+};
+template <int MC, int U, class V>
+__device__ __forceinline__ void u2trip_load(U2Trip<MC, U, V> &r, const ProjArgs &a, int64_t i0, int64_t stride,
+                                            int64_t nv, int deff, unsigned long long pk) {
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+        const int64_t i = i0 + u * stride;
+        const bool ok = i < nv;
+        r.ax[u] = ok ? ldp<V>(a.Ax, i, pk) : vzero(V());
+#pragma unroll
+        for (int k = 0; k < MC; ++k) r.col[u][k] = (ok && k < deff) ? ldp<V>(a.Bt + k * a.ld, i, pk) : vzero(V());
+    }
+}
+template <int MC, int U, class V, class CP>
+__device__ __forceinline__ void u2trip_compute(const U2Trip<MC, U, V> &r, CP c1, double (&v)[MC + 1]) {
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+        V b1 = r.ax[u];  // b1 = Ax - B~ c1 (registers only)
+#pragma unroll
+        for (int k = 0; k < MC; ++k) b1 = vaxpy(-c1[k], r.col[u][k], b1);
+#pragma unroll
+        for (int k = 0; k < MC; ++k) v[k] = vdot(r.col[u][k], b1, v[k]);
+        v[MC] = vdot(b1, b1, v[MC]);
+    }
+}
+
+// For MC >= 32 (SPLIT) a trip holds only Ax, x and the B~ columns; the X~ columns are loaded
+// (all at once) after the B~ part is finished, so the two 32-column register sets are never live
+// together and the pass can use 16-byte loads (VEC = 2) within the register file.
+template <int MC, int U, class V> struct U3Trip {  // update pass 3: U strided elements
+    static constexpr bool SPLIT = MC >= 32;
+    V ax[U], xv[U];
+    V bc[U][MC];
+    V xc[U][SPLIT ? 1 : MC];
+};
+template <int MC, class V>
+__device__ __forceinline__ void u3_load_x(V (&xc)[MC], const ProjArgs &a, int64_t i, bool ok, int nX,
+                                          unsigned long long ps) {
+#pragma unroll
+    for (int k = 0; k < MC; ++k) xc[k] = (ok && k < nX) ? ldp<V>(a.Xt + k * a.ld, i, ps) : vzero(V());
+}
+// Loads assume the pair is admitted (the common case); if it is not, the prefetched B~/Ax/x
+// values of that one trip are simply unused.
+template <int MC, int U, class V>
+__device__ __forceinline__ void u3trip_load(U3Trip<MC, U, V> &r, const ProjArgs &a, int64_t i0, int64_t stride,
+                                            int64_t nv, int deff, bool rotX, bool adm, unsigned long long ps) {
+    const int nB = adm ? deff : 0;
+    const int nX = rotX ? a.M : nB;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+        const int64_t i = i0 + u * stride;
+        const bool ok = i < nv;
+        r.ax[u] = (ok && adm) ? ldp<V>(a.Ax, i, ps) : vzero(V());
+        r.xv[u] = (ok && adm) ? ldp<V>(a.x, i, ps) : vzero(V());
+#pragma unroll
+        for (int k = 0; k < MC; ++k) r.bc[u][k] = (ok && k < nB) ? ldp<V>(a.Bt + k * a.ld, i, ps) : vzero(V());
+        if constexpr (!U3Trip<MC, U, V>::SPLIT) u3_load_x<MC, V>(r.xc[u], a, i, ok, nX, ps);
+    }
+}
+template <int MC, class V, class CP>
+__device__ __forceinline__ void u3_x_part(const V (&xc)[MC], const ProjArgs &a, int64_t i, bool rotX, V &xt, V &t2,
+                                          CP c1, CP c2, CP gc, CP gs, unsigned long long ps) {
+    if (rotX) {
+        V t = xc[0];
+#pragma unroll
+        for (int k = 0; k < MC - 1; ++k) {
+            if (k < a.M - 1) {
+                V nk;
+                vrot(gc[k], gs[k], t, xc[k + 1], nk);
+                stp<V>(a.Xt + k * a.ld, i, nk, ps);
+                xt = vaxpy(-c1[k], nk, xt);
+                t2 = vaxpy(c2[k], nk, t2);
+            }
+        }
+    } else {
+#pragma unroll
+        for (int k = 0; k < MC; ++k) {
+            xt = vaxpy(-c1[k], xc[k], xt);
+            t2 = vaxpy(c2[k], xc[k], t2);
+        }
+    }
+}
+template <int MC, int U, class V, class CP>
+__device__ __forceinline__ void u3trip_store(const U3Trip<MC, U, V> &r, const ProjArgs &a, int64_t i0,
+                                             int64_t stride, int64_t nv, int deff, bool rotX, bool adm, double inv,
+                                             CP c1, CP c2, CP gc, CP gs, unsigned long long ps) {
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+        const int64_t i = i0 + u * stride;
+        if (i >= nv) break;
+        // b~ = (Ax - B~ c1) - B~ c2 ; x~ = (x - X~ c1) - X~ c2 (separate corrections, DESIGN.md AMB-7)
+        V b1 = r.ax[u], s2 = vzero(V());
+#pragma unroll
+        for (int k = 0; k < MC; ++k) b1 = vaxpy(-c1[k], r.bc[u][k], b1);
+#pragma unroll
+        for (int k = 0; k < MC; ++k) s2 = vaxpy(c2[k], r.bc[u][k], s2);
+        if (adm) stp<V>(a.Bt + deff * a.ld, i, vscale(inv, vaxpy(-1.0, s2, b1)), ps);
+        V xt = r.xv[u], t2 = vzero(V());
+        if constexpr (U3Trip<MC, U, V>::SPLIT) {
+            V xc[MC];
+            u3_load_x<MC, V>(xc, a, i, true, rotX ? a.M : (adm ? deff : 0), ps);
+            u3_x_part<MC, V>(xc, a, i, rotX, xt, t2, c1, c2, gc, gs, ps);
+        } else {
+            u3_x_part<MC, V>(r.xc[u], a, i, rotX, xt, t2, c1, c2, gc, gs, ps);
+        }
+        if (adm) stp<V>(a.Xt + deff * a.ld, i, vscale(inv, vaxpy(-1.0, t2, xt)), ps);
+    }
+}
 
 // One warp: Givens parameters of the next downdate from R (AMB-2 reading of P:279-290):
 // H = R_{:,2:M}; for i: a = H_ii, b = H_{i+1,i}, r = hypot(a,b), c = a/r, s = b/r; rotate rows.
