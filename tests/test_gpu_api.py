@@ -48,6 +48,30 @@ def test_byte_accounting_follows_the_fused_schedule():
         d_before = ig.d
     # steady state: (8M+4) values per element per step
     assert fb + ub == (8 * M + 4) * vb
+    # against the paper's Table 1 (tests/golden/paper_values.txt): the guess moves
+    # exactly 2(M+1)N values; the update moves at most the table's (10M+24)N minus the 9N operator
+    # apply that is not part of the library (the fused Givens sweep saves the rest)
+    assert fb == 2 * (M + 1) * vb
+    assert ub <= (10 * M + 24 - 9) * vb
+    ig.close()
+
+
+def test_extrapolation_bytes_match_table_1():
+    """EXTRAP(m, M): (M+1)N per step with the solver writing in place."""
+    from paper_2009_10863_b200 import InitialGuess
+
+    N, M, m = 5000, 8, 2  # EXTRAP(2,8): all weights nonzero
+    ig = InitialGuess(N, "extrap_ls", M, m)
+    assert all(w != 0.0 for w in ig.weights())
+    for n in range(M + 2):
+        slot = ig.next_slot()
+        if n == 0:
+            slot.zero_()
+        ig.form_guess(None, slot)
+        slot.add_(1.0)  # the "solver" writes its solution in place
+        ig.update(slot)
+    fb, ub = ig.bytes()
+    assert fb == (M + 1) * 8 * N and ub == 0
     ig.close()
 
 
