@@ -16,6 +16,18 @@
 
 #include "proj_common.cuh"
 
+// Phase timestamps per CTA (debug builds with -DIG_TRACE=1; IG_TRACE_PTR = device buffer address
+// passed through the environment at launch): [cta][slot] = %globaltimer.
+#ifdef IG_TRACE
+__device__ unsigned long long g_trace[1024 * 8];
+#define TRACE(slot) do { if (threadIdx.x == 0) g_trace[blockIdx.x * 8 + (slot)] = globaltimer_ns(); } while (0)
+extern "C" int ig_debug_trace_read(unsigned long long *host, int n) {
+    return (int)cudaMemcpyFromSymbol(host, g_trace, sizeof(unsigned long long) * n);
+}
+#else
+#define TRACE(slot) do { } while (0)
+#endif
+
 namespace ig {
 
 // Second block-partial buffer so that a fast CTA's pass-2 partials never overwrite pass-1
@@ -116,6 +128,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_update_fused(ProjArgs a) {
     const int deff = pend ? M - 1 : (restart ? 0 : d);
     const unsigned long long ep1 = c->xepoch[ST_U1] + 1, ep2 = c->xepoch[ST_U2] + 1;
     const L2Pol pol = make_l2pol();
+    TRACE(0);
     if (threadIdx.x < MAXM) {
         const bool rot = pend && threadIdx.x < M - 1;
         s_gc[threadIdx.x] = rot ? c->gc[threadIdx.x] : 1.0;
@@ -153,8 +166,11 @@ __global__ void __launch_bounds__(THREADS, 1) k_update_fused(ProjArgs a) {
     U2Trip<MC, UB, V> pre2;
     if (deff > 0 && ntrip2 > 0) u2trip_load(pre2, a, i_first + (ntrip2 - 1) * UB * stride, stride, nv, deff, pol.keep);
     block_partials_store<MC + 1>(v, deff, true, a.blk, sh);
+    TRACE(1);
     grid_barrier(&c->bar, 1, &c->err, a.watchdog_ns);
+    TRACE(2);
     reduce_all_blocks<MC>(deff, true, a.blk, s_r1);
+    TRACE(3);
     if (a.xc.G > 1) peer_allreduce(a.xc, ST_U1, deff, true, s_r1, ep1, &c->err, a.watchdog_ns);
     if (threadIdx.x < MAXM) s_c1[threadIdx.x] = (threadIdx.x < deff) ? s_r1[threadIdx.x] : 0.0;
     __syncthreads();
@@ -181,7 +197,9 @@ __global__ void __launch_bounds__(THREADS, 1) k_update_fused(ProjArgs a) {
     U3Trip<MC, U3, V> pre3;  // first trip of pass 3, in flight across barrier 2
     u3trip_load(pre3, a, i_first, stride, nv, deff, pend, true, pol.stream);
     if (deff > 0) block_partials_store<MC + 1>(v, deff, true, a.blk + BLK2, sh);
+    TRACE(4);
     grid_barrier(&c->bar, 2, &c->err, a.watchdog_ns);
+    TRACE(5);
     if (deff > 0) reduce_all_blocks<MC>(deff, true, a.blk + BLK2, s_r2);
     if (deff > 0 && a.xc.G > 1) peer_allreduce(a.xc, ST_U2, deff, true, s_r2, ep2, &c->err, a.watchdog_ns);
     if (threadIdx.x == 0) {
@@ -222,11 +240,13 @@ __global__ void __launch_bounds__(THREADS, 1) k_update_fused(ProjArgs a) {
             u3trip_store(r, a, a.N - 1, 1, a.N, deff, pend, adm, inv, c1, c2, gc, gs, pol.stream);
         }
     }
+    TRACE(6);
     pdl_trigger();
     // ---- epilogue (last CTA out): control block, R, next downdate's Givens
     if (!grid_exit(&c->bar, &c->bar_exit)) return;
     if (pend)
-        for (int idx = threadIdx.x; idx < MAXM * MAXM; idx += blockDim.x) c->R[idx] = c->Rdn[idx];
+        for (int idx = threadIdx.x; idx < M * M; idx += blockDim.x)  // leading M x M block only
+            c->R[(idx % M) + (idx / M) * MAXM] = c->Rdn[(idx % M) + (idx / M) * MAXM];
     __syncthreads();
     const int dnew = deff + (adm ? 1 : 0);
     if (a.method == M_PROJ_QR && adm) {  // R_{1:d,d+1} = c1 + c2, R_{d+1,d+1} = ||b~||

@@ -143,7 +143,8 @@ __global__ void __launch_bounds__(THREADS, 1) k_u1(ProjArgs a) {
     if (block_partials_ticket<MC + 1>(v, deff, true, a.blk, &c->ticket[ST_U1], sh)) {
         final_reduce<MC>(deff, true, a.blk, a.part + ST_U1 * PS);
         if (pend)
-            for (int idx = threadIdx.x; idx < MAXM * MAXM; idx += blockDim.x) c->R[idx] = c->Rdn[idx];
+            for (int idx = threadIdx.x; idx < M * M; idx += blockDim.x)  // leading M x M block only
+                c->R[(idx % M) + (idx / M) * MAXM] = c->Rdn[(idx % M) + (idx / M) * MAXM];
         if (threadIdx.x == 0) {
             c->deff = deff;
             c->rotX = pend ? 1 : 0;

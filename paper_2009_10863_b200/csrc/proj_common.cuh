@@ -565,11 +565,11 @@ __device__ __forceinline__ void u3trip_store(const U3Trip<MC, U, V> &r, const Pr
 // One warp: Givens parameters of the next downdate from R (AMB-2 reading of P:279-290):
 // H = R_{:,2:M}; for i: a = H_ii, b = H_{i+1,i}, r = hypot(a,b), c = a/r, s = b/r; rotate rows.
 static __device__ __noinline__ void givens_plan(Ctrl *c, int M, double *H) {
-    const int lane = threadIdx.x & 31;
-    for (int idx = lane; idx < MAXM * MAXM; idx += 32) {
-        const int i = idx / MAXM, j = idx % MAXM;
-        H[idx] = (i < M && j < M - 1) ? c->R[i + (j + 1) * MAXM] : 0.0;
-    }
+    // Only the leading M x M block of R / Rdn is ever read: touch nothing else (this runs in
+    // the serial tail of the update kernel).  Lane j owns column j of H.
+    const int lane = threadIdx.x & 31, j = lane;
+    if (j < M - 1)
+        for (int i = 0; i < M; ++i) H[i * MAXM + j] = c->R[i + (j + 1) * MAXM];
     __syncwarp();
     for (int i = 0; i < M - 1; ++i) {
         const double aa = H[i * MAXM + i], bb = H[(i + 1) * MAXM + i];
@@ -577,7 +577,6 @@ static __device__ __noinline__ void givens_plan(Ctrl *c, int M, double *H) {
         const double cs = (r == 0.0) ? 1.0 : aa / r;
         const double sn = (r == 0.0) ? 0.0 : bb / r;
         __syncwarp();
-        const int j = lane;
         if (j >= i && j < M - 1) {
             const double hi = H[i * MAXM + j], hi1 = H[(i + 1) * MAXM + j];
             H[i * MAXM + j] = cs * hi + sn * hi1;
@@ -589,10 +588,8 @@ static __device__ __noinline__ void givens_plan(Ctrl *c, int M, double *H) {
         }
         __syncwarp();
     }
-    for (int idx = lane; idx < MAXM * MAXM; idx += 32) {
-        const int i = idx % MAXM, j = idx / MAXM;  // column-major destination
-        c->Rdn[idx] = (i < M - 1 && j < M - 1 && i <= j) ? H[i * MAXM + j] : 0.0;
-    }
+    if (j < M)  // column-major destination, leading M x M block
+        for (int i = 0; i < M; ++i) c->Rdn[i + j * MAXM] = (i < M - 1 && j < M - 1 && i <= j) ? H[i * MAXM + j] : 0.0;
     __syncwarp();
     if (lane == 0) c->pending = 1;
 }
