@@ -47,6 +47,7 @@ struct Ctrl {
     int err;        // device watchdog: 0 ok, 1 grid-barrier timeout, 2 peer-exchange timeout
     unsigned ticket[NSTAGE];
     unsigned bar, bar_exit;        // grid barrier / exit counters of the fused kernels
+    unsigned dyn3, dyn_pad_;       // work-claim counter of the dynamically balanced pass-3 tail
     unsigned long long xepoch[NSTAGE];  // completed peer exchanges per stage (all ranks agree)
     double rho, nAx, nb;
     double gc[MAXM], gs[MAXM];      // Givens (c_i, s_i) of the pending downdate

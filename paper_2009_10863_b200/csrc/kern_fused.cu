@@ -228,11 +228,33 @@ __global__ void __launch_bounds__(THREADS, 1) k_update_fused(ProjArgs a) {
     }
     // ---- pass 3: [Givens rotation of X~] + store the admitted pair
     if (adm || pend) {
-        u3trip_store(pre3, a, i_first, stride, nv, deff, pend, adm, inv, c1, c2, gc, gs, pol.stream);
-        for (int64_t i0 = i_first + U3 * stride; i0 < nv; i0 += U3 * stride) {
+        // ~7/8 of the trips in the static grid-stride order (trip 0 is the prefetched pre3), the
+        // last ~1/8 of the rows handed out to warps on demand (32*U3-row chunks, atomic claim):
+        // CTAs on slower SMs take fewer tail chunks, so all CTAs reach the exit together.
+        const int64_t chunk = (int64_t)U3 * stride;
+        const int64_t trips = (nv + chunk - 1) / chunk;
+        const int64_t Ts = trips < 4 ? trips : trips - (trips + 7) / 8;
+        if (Ts > 0) u3trip_store(pre3, a, i_first, stride, nv, deff, pend, adm, inv, c1, c2, gc, gs, pol.stream);
+        for (int64_t t = 1; t < Ts; ++t) {
+            const int64_t i0 = i_first + t * chunk;
             U3Trip<MC, U3, V> r;
             u3trip_load(r, a, i0, stride, nv, deff, pend, adm, pol.stream);
             u3trip_store(r, a, i0, stride, nv, deff, pend, adm, inv, c1, c2, gc, gs, pol.stream);
+        }
+        const int64_t S = Ts * chunk, WCH = 32 * U3;
+        const int64_t nq = nv > S ? (nv - S + WCH - 1) / WCH : 0;
+        if (nq > 0) {
+            const int lane = threadIdx.x & 31;
+            unsigned q = (lane == 0) ? atomicAdd(&c->dyn3, 1u) : 0u;
+            q = __shfl_sync(0xffffffffu, q, 0);
+            while ((int64_t)q < nq) {
+                unsigned qn = (lane == 0) ? atomicAdd(&c->dyn3, 1u) : 0u;  // claim the next one early
+                const int64_t i0 = S + (int64_t)q * WCH + lane;
+                U3Trip<MC, U3, V> r;
+                u3trip_load(r, a, i0, 32, nv, deff, pend, adm, pol.stream);
+                u3trip_store(r, a, i0, 32, nv, deff, pend, adm, inv, c1, c2, gc, gs, pol.stream);
+                q = __shfl_sync(0xffffffffu, qn, 0);
+            }
         }
         if (tail) {
             U3Trip<MC, 1, double> r;
@@ -259,6 +281,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_update_fused(ProjArgs a) {
     }
     __syncthreads();
     if (threadIdx.x == 0) {
+        c->dyn3 = 0;  // every other CTA has left: no claims in flight
         c->d = dnew;
         c->deff = deff;
         c->pending = 0;
