@@ -77,7 +77,7 @@ SCHEDULES = [pytest.param(True, id="fused"), pytest.param(False, id="split")]
 
 
 @pytest.mark.parametrize("fused", SCHEDULES)
-@pytest.mark.parametrize("M", [1, 2, 3, 5, 8, 12, 16, 30])
+@pytest.mark.parametrize("M", [1, 2, 3, 5, 8, 12, 16, 30, 32])
 def test_proj_qr_open_loop_c1(M, fused):
     # configs[0]: 2D 32x32 5-point Helmholtz, 40 steps
     run_proj_parity(Grid(32, 2), M, 40, fused=fused)
@@ -466,3 +466,46 @@ def test_admission_tolerance_parity(eps):
     if eps >= 1e-4:
         assert max(ds) < 6  # the tolerance really rejected pairs
     ig.close()
+
+
+# ------------------------------------------------------------------ full-size properties (configs[2] scale)
+@pytest.mark.slow
+def test_properties_at_2_27_dofs():
+    """configs[2] size (2^27 DOFs) in the bench launch configuration, where the oracle cannot run
+    whole: properties that hold at any size -- B~ orthonormal, b = B~_j gives
+    x0 = X~_j, and extrapolation sampled element by element against Eq. EXTRAPEXPN
+    with the oracle's exact-rational weights."""
+    from paper_2009_10863_b200 import InitialGuess, ig_copy_history
+
+    N, M = 1 << 27, 4
+    gen = torch.Generator(device="cuda").manual_seed(10863)
+    ig = InitialGuess(N, "proj_qr", M)
+    ie = InitialGuess(N, "extrap_ls", M, 2)
+    xs = []
+    for _ in range(M + 2):
+        x = torch.randn(N, dtype=torch.float64, device="cuda", generator=gen)
+        Ax = torch.randn(N, dtype=torch.float64, device="cuda", generator=gen)
+        ig.update(x, Ax)
+        ie.update(x)
+        xs.append(x)
+    assert ig.d == M
+    Bt, Xt, _ = ig_copy_history(ig.h, M, N)
+    G = Bt @ Bt.T
+    assert torch.max(torch.abs(G - torch.eye(M, dtype=torch.float64, device="cuda"))).item() <= 1e-12
+    for j in range(M):
+        x0 = torch.zeros(N, dtype=torch.float64, device="cuda")
+        ig.form_guess(Bt[j].contiguous(), x0)
+        err = torch.linalg.vector_norm(x0 - Xt[j]) / torch.linalg.vector_norm(Xt[j])
+        assert err.item() <= 1e-11
+    x0 = torch.zeros(N, dtype=torch.float64, device="cuda")
+    ie.form_guess(None, x0)
+    beta = warmup_weights(2, M, M)
+    idx = torch.randint(0, N, (4096,), generator=gen, device="cuda")
+    window = torch.stack([xs[-M + k][idx] for k in range(M)]).cpu().numpy()
+    ref = np.zeros(idx.numel())
+    for k in range(M):  # Eq. EXTRAPEXPN, oldest first, one element at a time
+        ref = ref + beta[k] * window[k]
+    got = x0[idx].cpu().numpy()
+    assert np.max(np.abs(got - ref)) <= 1e-13 * np.max(np.abs(ref)) * np.abs(beta).sum()
+    ig.close()
+    ie.close()
