@@ -135,6 +135,17 @@ int ig_update_host(ig_t h, const double *x, const double *Ax);
  * ig_form_guess).  NULL for projection methods. */
 double *ig_next_slot(ig_t h);
 
+/* ---------------------------------------------------------------- checkpoint / resume */
+
+/* Host-memory image of one history space (B~, X~, R and the device control block for
+ * projection; the solution window, its order and fill for extrapolation) for restarting a long
+ * run.  ig_save_state / ig_load_state sync the handle's stream; the image is only valid for a
+ * handle created with the same (N, method, m, degree) on any device.  Multi-rank handles save
+ * their local shard; all ranks must load images saved at the same step. */
+size_t ig_state_bytes(ig_t h);
+int ig_save_state(ig_t h, void *host_buf, size_t bytes);
+int ig_load_state(ig_t h, const void *host_buf, size_t bytes);
+
 /* ---------------------------------------------------------------- multi-GPU */
 
 /* Write a fresh NCCL unique id (128 bytes) into out (call on one rank, broadcast the bytes). */

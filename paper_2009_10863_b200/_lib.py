@@ -36,6 +36,9 @@ _SIGS = {
     "ig_set_stream": (C.c_int, [_P, _P]),
     "ig_set_admit_tol": (C.c_int, [_P, C.c_double]),
     "ig_set_schedule": (C.c_int, [_P, C.c_int]),
+    "ig_state_bytes": (C.c_size_t, [_P]),
+    "ig_save_state": (C.c_int, [_P, _P, C.c_size_t]),
+    "ig_load_state": (C.c_int, [_P, _P, C.c_size_t]),
     "ig_form_guess": (C.c_int, [_P, _P, _P]),
     "ig_update": (C.c_int, [_P, _P, _P]),
     "ig_form_guess_host": (C.c_int, [_P, _P, _P]),

@@ -430,6 +430,75 @@ int ig_reset(ig_t h) {
     return IG_OK;
 }
 
+namespace {
+struct StateHeader {
+    uint64_t magic;  // "IGSTATE1"
+    int32_t method, M, degree, head;
+    int64_t N;
+    int32_t fill, nslab;
+    double eps;
+};
+const uint64_t STATE_MAGIC = 0x3145544154534749ull;  // "IGSTATE1" little-endian
+int nslabs(ig_t h) { return is_proj(h->method) ? 2 * h->M : h->M; }
+}  // namespace
+
+size_t ig_state_bytes(ig_t h) {
+    if (!h) return 0;
+    return sizeof(StateHeader) + (is_proj(h->method) ? sizeof(Ctrl) : 0) +
+           sizeof(double) * (size_t)nslabs(h) * (size_t)h->N;
+}
+
+int ig_save_state(ig_t h, void *host_buf, size_t bytes) {
+    if (!h || !host_buf || bytes < ig_state_bytes(h)) return set_err(IG_E_ARG, "bad handle or buffer too small");
+    DevGuard g(h->dev);
+    char *p = static_cast<char *>(host_buf);
+    StateHeader hd = {STATE_MAGIC, h->method, h->M, h->degree, h->head, h->N, h->fill, nslabs(h), h->eps};
+    memcpy(p, &hd, sizeof hd);
+    p += sizeof hd;
+    if (is_proj(h->method)) {
+        CUDA_OK(cudaMemcpyAsync(p, h->ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, h->stream));
+        p += sizeof(Ctrl);
+    }
+    const size_t w = sizeof(double) * (size_t)h->N;
+    CUDA_OK(cudaMemcpy2DAsync(p, w, h->slab, sizeof(double) * h->ld, w, nslabs(h), cudaMemcpyDeviceToHost,
+                              h->stream));
+    CUDA_OK(cudaStreamSynchronize(h->stream));
+    return IG_OK;
+}
+
+int ig_load_state(ig_t h, const void *host_buf, size_t bytes) {
+    if (!h || !host_buf || bytes < sizeof(StateHeader)) return set_err(IG_E_ARG, "bad handle or buffer");
+    DevGuard g(h->dev);
+    const char *p = static_cast<const char *>(host_buf);
+    StateHeader hd;
+    memcpy(&hd, p, sizeof hd);
+    if (hd.magic != STATE_MAGIC) return set_err(IG_E_ARG, "not an ig state image");
+    if (hd.method != h->method || hd.M != h->M || hd.degree != h->degree || hd.N != h->N)
+        return set_err(IG_E_ARG, "state image is for (method %d, N %lld, m %d, degree %d)", hd.method,
+                       (long long)hd.N, hd.M, hd.degree);
+    if (bytes < ig_state_bytes(h)) return set_err(IG_E_ARG, "state image truncated");
+    p += sizeof hd;
+    if (is_proj(h->method)) {
+        Ctrl c;
+        memcpy(&c, p, sizeof c);
+        for (unsigned &t : c.ticket) t = 0;  // transient launch state is never part of a checkpoint
+        c.bar = c.bar_exit = c.dyn3 = 0;
+        c.err = 0;
+        CUDA_OK(cudaMemcpyAsync(h->ctrl, &c, sizeof c, cudaMemcpyHostToDevice, h->stream));
+        CUDA_OK(cudaStreamSynchronize(h->stream));  // c is a stack object
+        p += sizeof(Ctrl);
+        h->known_d = -1;
+    }
+    const size_t w = sizeof(double) * (size_t)h->N;
+    CUDA_OK(cudaMemcpy2DAsync(h->slab, sizeof(double) * h->ld, p, w, w, nslabs(h), cudaMemcpyHostToDevice,
+                              h->stream));
+    CUDA_OK(cudaStreamSynchronize(h->stream));
+    h->head = hd.head;
+    h->fill = hd.fill;
+    h->eps = hd.eps;
+    return IG_OK;
+}
+
 int ig_form_guess(ig_t h, const double *b, double *x0) {
     if (!h) return set_err(IG_E_ARG, "NULL handle");
     if (!x0) return set_err(IG_E_ARG, "x0 is NULL");
@@ -770,6 +839,9 @@ static int watchdog_error(int err) {
     if (err == 2)
         return set_err(IG_E_STATE, "device watchdog: the peer exchange timed out (a rank stopped calling?); "
                                    "the history is invalid, ig_reset every rank");
+    if (err == 3)
+        return set_err(IG_E_STATE, "non-finite projection sums (NaN/Inf in b, x or A x?); the pair was not "
+                                   "admitted -- check the inputs");
     return IG_OK;
 }
 

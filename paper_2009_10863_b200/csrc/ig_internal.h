@@ -44,7 +44,7 @@ struct Ctrl {
     int deff;       // dimension the Gram-Schmidt passes of the current update use
     int admitted;   // last update admitted its pair
     int last_rot;   // the last update applied a downdate (bytes accounting)
-    int err;        // device watchdog: 0 ok, 1 grid-barrier timeout, 2 peer-exchange timeout
+    int err;        // failure detection: 0 ok, 1 grid-barrier / 2 peer-exchange timeout, 3 non-finite sums
     unsigned ticket[NSTAGE];
     unsigned bar, bar_exit;        // grid barrier / exit counters of the fused kernels
     unsigned dyn3, dyn_pad_;       // work-claim counter of the dynamically balanced pass-3 tail

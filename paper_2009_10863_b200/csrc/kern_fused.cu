@@ -104,6 +104,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_form_fused(ProjArgs a) {
     pdl_trigger();
     if (grid_exit(&c->bar, &c->bar_exit)) {
         if (threadIdx.x < d) a.part[ST_FORM * PS + threadIdx.x] = s_red[threadIdx.x];
+        if (threadIdx.x < d && !isfinite(s_red[threadIdx.x])) watchdog_trip(&c->err, 3);
         if (threadIdx.x == 0 && a.xc.G > 1) c->xepoch[ST_FORM] = ep;
     }
 }
@@ -281,6 +282,10 @@ __global__ void __launch_bounds__(THREADS, 1) k_update_fused(ProjArgs a) {
     }
     __syncthreads();
     if (threadIdx.x == 0) {
+        // failure detection: non-finite inputs poison the sums (the pair is then not admitted)
+        bool fin = isfinite(s_r1[NORM]) && (deff == 0 || isfinite(s_r2[NORM]));
+        for (int k = 0; k < deff; ++k) fin = fin && isfinite(s_r1[k]) && isfinite(s_r2[k]);
+        if (!fin) watchdog_trip(&c->err, 3);
         c->dyn3 = 0;  // every other CTA has left: no claims in flight
         c->d = dnew;
         c->deff = deff;

@@ -274,6 +274,9 @@ __global__ void __launch_bounds__(THREADS, 1) k_u3(ProjArgs a) {
     }
     __syncthreads();
     if (threadIdx.x == 0) {
+        bool fin = isfinite(s_nb) && isfinite(s_nAx);
+        for (int k = 0; k < deff; ++k) fin = fin && isfinite(s_c1[k]) && isfinite(s_c2[k]);
+        if (!fin) watchdog_trip(&c->err, 3);
         c->d = dnew;
         c->admitted = adm ? 1 : 0;
         c->nb = s_nb;

@@ -258,6 +258,18 @@ def comm_from_process_group(group=None):
     return ig_comm_create(world, rank, obj[0])
 
 
+def ig_save_state(h) -> bytes:
+    """Checkpoint image of one history space (host bytes)."""
+    n = int(lib().ig_state_bytes(h))
+    buf = (C.c_char * n)()
+    _check(lib().ig_save_state(h, buf, n), "ig_save_state")
+    return bytes(buf)
+
+
+def ig_load_state(h, image: bytes) -> None:
+    _check(lib().ig_load_state(h, C.c_char_p(image), len(image)), "ig_load_state")
+
+
 def ig_set_grid_limit(h, max_blocks: int) -> None:
     _check(lib().ig_set_grid_limit(h, int(max_blocks)), "ig_set_grid_limit")
 
@@ -382,6 +394,12 @@ class InitialGuess:
 
     def weights(self, f: int = 0):
         return ig_weights(self.h, f)
+
+    def save_state(self) -> bytes:
+        return ig_save_state(self.h)
+
+    def load_state(self, image: bytes) -> None:
+        ig_load_state(self.h, image)
 
     def reset(self):
         ig_reset(self.h)

@@ -157,3 +157,50 @@ def test_argument_errors_on_device():
     with pytest.raises(IGError, match="Ax is NULL"):
         ig.update(torch.zeros(100, dtype=torch.float64, device="cuda"), None)
     ig.close()
+
+
+@pytest.mark.parametrize("method,M,p", [("proj_qr", 6, 0), ("proj_classic", 4, 0), ("extrap_ls", 6, 3),
+                                        ("extrap_sparse", 8, 2)])
+def test_checkpoint_resume_is_bitwise(method, M, p):
+    """Save the history mid-run, load it into a fresh handle: the resumed run reproduces the
+    uninterrupted one bit for bit."""
+    from paper_2009_10863_b200 import IGError, InitialGuess
+
+    g = Grid(30, 2)
+    seq = _seq(g, 2 * M + 6)
+    a = InitialGuess(g.N, method, M, p)
+    half = M + 2
+    for b, x, Ax in seq[:half]:
+        a.update(torch.from_numpy(x).cuda(), torch.from_numpy(Ax).cuda())
+    img = a.save_state()
+    bnew = InitialGuess(g.N, method, M, p)
+    bnew.load_state(img)
+    for b, x, Ax in seq[half:]:
+        outs = []
+        for h in (a, bnew):
+            x0 = torch.zeros(g.N, dtype=torch.float64, device="cuda")
+            h.form_guess(torch.from_numpy(b).cuda(), x0)
+            outs.append(x0.cpu().numpy())
+            h.update(torch.from_numpy(x).cuda(), torch.from_numpy(Ax).cuda())
+        assert np.array_equal(outs[0], outs[1])
+    other = InitialGuess(g.N + 1, method, M, p)
+    with pytest.raises(IGError, match="state image is for"):
+        other.load_state(img)
+    for h in (a, bnew, other):
+        h.close()
+
+
+@pytest.mark.parametrize("fused", [True, False])
+def test_non_finite_inputs_are_reported(fused):
+    from paper_2009_10863_b200 import IGError, InitialGuess
+
+    N = 4000
+    ig = InitialGuess(N, "proj_qr", 4, fused=fused)
+    x = torch.rand(N, dtype=torch.float64, device="cuda")
+    ig.update(x, x + 1.0)
+    bad = x.clone()
+    bad[17] = float("nan")
+    ig.update(bad, bad)
+    with pytest.raises(IGError, match="non-finite"):
+        ig.stats()
+    ig.close()
