@@ -41,8 +41,11 @@ def parse():
     p.add_argument("--steps", type=int, default=200)
     p.add_argument("--warmup", type=int, default=10)
     p.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    p.add_argument("--n", type=int, default=128, help="grid points per direction (per-GPU slab n^3)")
-    p.add_argument("--m", type=int, default=8, help="history size M (projection and extrapolation)")
+    p.add_argument("--config", choices=["c2", "c3", "c4"], default="c2",
+                   help="c2 (default): configs[1] 128^3 QR(8)+EXTRAP(3,8); c3: configs[2] 512^3 (2^27 DOFs) QR(m); "
+                        "c4: configs[3] 2^28 DOFs/GPU QR(16)+EXTRAP(3,16)")
+    p.add_argument("--n", type=int, default=None, help="grid points per direction (per-GPU slab n^3), overrides --config")
+    p.add_argument("--m", type=int, default=None, help="history size M (projection and extrapolation)")
     p.add_argument("--degree", type=int, default=3, help="extrapolation degree")
     p.add_argument("--e2e-steps", type=int, default=20)
     p.add_argument("--no-cpu-baseline", action="store_true")
@@ -51,7 +54,17 @@ def parse():
                    help="TEST MODE: all ranks on GPU 0 (gloo plumbing, 1/N of the SMs each) to exercise the N>1 path")
     p.add_argument("--exchange", choices=["peer", "nccl"], default="peer",
                    help="N>1 projection sums: in-kernel NVLink peer exchange (fused) or NCCL between kernels")
-    return p.parse_args()
+    a = p.parse_args()
+    # (nx, ny, nz per GPU, M): the z extent is per rank (contiguous z-slabs, weak scaling)
+    shape = {"c2": (128, 128, 128, 8), "c3": (512, 512, 512, 8), "c4": (512, 512, 1024, 16)}[a.config]
+    if a.n is not None:
+        shape = (a.n, a.n, a.n, shape[3])
+    a.nxy, a.nz = shape[0], shape[2]
+    a.n = a.nxy
+    if a.m is None:
+        a.m = shape[3]
+    a.cfg_name = {"c2": "C2 configs[1]", "c3": "C3 configs[2]", "c4": "C4 configs[3]"}[a.config]
+    return a
 
 
 def peak_hbm():
@@ -224,17 +237,19 @@ def run_reference(args, world, rank):
     """--impl reference: the oracle timed on the host cores (rank 0 only)."""
     if rank != 0:
         return
-    n, M, p = args.n, args.m, args.degree
-    nz = max(1, n // 8)
+    n, M, p = args.nxy, args.m, args.degree
+    N_full = n * n * args.nz
+    nz = max(1, (1 << 18) // (n * n))  # a ~262K-DOF contiguous z-slab sample of the workload
     # warm-up steps double as history fill; each timed step is one oracle step on the sample
     sps, bps, done, Ns = oracle_sample_run(n, M, p, nz, args.steps, None, max(args.warmup, M + 1))
     gbs = bps / sps / 1e9
-    sample = (f"{nz} of {n} z-planes of the {n}^3 C2 grid ({Ns} DOFs), QR({M}) + EXTRAP({p},{M}) oracle steps, "
-              f"{done} timed after {max(args.warmup, M + 1)} fill steps")
+    sample = (f"{nz} of {args.nz} z-planes of the {n}x{n}x{args.nz} {args.cfg_name} grid ({Ns} DOFs), "
+              f"QR({M}) + EXTRAP({p},{M}) oracle steps, {done} timed after {max(args.warmup, M + 1)} fill steps")
     out = {"metric": METRIC, "value": gbs, "unit": "GB/s", "n_gpus": args.gpus, "steps": args.steps,
-           "warmup": args.warmup, "ms_per_step": sps * 1e3 * (n // nz), "higher_is_better": True,
+           "warmup": args.warmup, "ms_per_step": sps * 1e3 * (N_full / Ns), "higher_is_better": True,
            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
-           "config": {"workload": f"C2 3D {n}^3 7-point Helmholtz manufactured sequence, QR({M}) + EXTRAP({p},{M})",
+           "config": {"workload": f"{args.cfg_name}: 3D {n}x{n}x{args.nz} 7-point Helmholtz manufactured sequence "
+                                  f"per GPU, QR({M}) + EXTRAP({p},{M})",
                       "sample": sample, "ms_per_step_note": "sample time scaled to the full grid"},
            "cpu_baseline": {"value": gbs, "unit": "GB/s", "cores": cpu_cores(), "kind": "oracle", "sample": sample},
            "e2e": {"value": gbs, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -249,15 +264,30 @@ def run_ours(args, world, rank, local):
                                        ig_profile_read, ig_total_launches, ig_update_host, peers_from_process_group)
     from workloads.gen import manufactured_step_slab
 
-    n, M, p = args.n, args.m, args.degree
-    N = n * n * n
+    n, M, p = args.nxy, args.m, args.degree
+    nz = args.nz
+    N = n * n * nz
     K, W = args.steps, args.warmup
     prefill = max(0, M + 1 - W)  # untimed history fill when W is too short to reach the steady state
     S = prefill + W + K
     dev = torch.device("cuda", local)
 
-    # ---- inputs resident in HBM before the timed region: one fresh (b, x, Ax) per step
-    pool = [manufactured_step_slab(n, n, rank, world, k, device=dev) for k in range(S)]
+    # ---- inputs resident in HBM before the timed region: one fresh (b, x, Ax) per step, or --
+    # when S steps of inputs would not fit next to the history (c3/c4) -- a pool of P = M+2
+    # distinct steps cycled (a pair re-enters only after it left the M-window: still admitted)
+    vec_gb = 8 * N / 1e9
+    cap_gb = 0.85 * torch.cuda.get_device_properties(dev).total_memory / 1e9
+    hist_gb = (3 * M + 4) * vec_gb  # QR slabs 2M, EXTRAP ring M, x0 buffers
+    if 3 * S * vec_gb + hist_gb < cap_gb:
+        P, regen = S, False
+    elif 3 * (M + 2) * vec_gb + hist_gb < cap_gb:
+        P, regen = M + 2, False
+    else:
+        # configs[3] (2^28 DOFs per GPU, M = 16): the history alone is ~110 GB, no input pool
+        # fits.  Inputs are regenerated into fixed buffers between steps, OUTSIDE the timed
+        # windows: every step is bracketed by its own events and the K windows are summed.
+        P, regen = 1, True
+    pool = [manufactured_step_slab(n, nz, rank, world, k, device=dev) for k in range(P)]
     torch.cuda.synchronize()
 
     comm = comm_from_process_group() if (world > 1 and args.exchange == "nccl") else None
@@ -278,14 +308,21 @@ def run_ours(args, world, rank, local):
     x0p = torch.zeros(N, dtype=torch.float64, device=dev)
     x0e = torch.zeros(N, dtype=torch.float64, device=dev)
 
+    def refill(k):  # regen mode: step k's inputs into the single pool slot (untimed)
+        for dst, src in zip(pool[0], manufactured_step_slab(n, nz, rank, world, k, device=dev)):
+            dst.copy_(src)
+            del src
+
     def step(k):
-        b, x, Ax = pool[k % S]
+        b, x, Ax = pool[k % P]
         hp.form_guess(b, x0p)
         hp.update(x, Ax)
         he.form_guess(None, x0e)
         he.update(x)
 
     for k in range(prefill + W):
+        if regen:
+            refill(k)
         step(k)
     torch.cuda.synchronize()
     assert hp.d == M, f"projection history not full after warm-up (d={hp.d})"
@@ -297,16 +334,31 @@ def run_ours(args, world, rank, local):
     torch.cuda.synchronize()
     l0 = ig_total_launches()
     with sampler:
-        e0.record(stream)
-        th0 = time.perf_counter()
-        for k in range(prefill + W, S):
-            step(k)
-        host_us = (time.perf_counter() - th0) / K * 1e6  # host enqueue cost per step (async launches)
-        e1.record(stream)
-        torch.cuda.synchronize()
+        if not regen:
+            e0.record(stream)
+            th0 = time.perf_counter()
+            for k in range(prefill + W, S):
+                step(k)
+            host_us = (time.perf_counter() - th0) / K * 1e6  # host enqueue cost per step (async launches)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            t_local = e0.elapsed_time(e1)
+        else:
+            t_local, host_us, launches_regen = 0.0, 0.0, 0
+            for k in range(prefill + W, S):
+                refill(k)
+                barrier(world)
+                torch.cuda.synchronize()
+                l1 = ig_total_launches()
+                e0.record(stream)
+                step(k)
+                e1.record(stream)
+                torch.cuda.synchronize()
+                launches_regen += ig_total_launches() - l1
+                t_local += e0.elapsed_time(e1)
     barrier(world)
-    launches = ig_total_launches() - l0
-    t_ms = max_over_ranks(e0.elapsed_time(e1), world)
+    launches = ig_total_launches() - l0 if not regen else launches_regen
+    t_ms = max_over_ranks(t_local, world)
     st = hp.stats()
     fb, ub = hp.bytes()
     nnz = sum(1 for w in he.weights() if w != 0.0)
@@ -324,6 +376,8 @@ def run_ours(args, world, rank, local):
     ig_profile(hp.h, True)
     ig_profile(he.h, True)
     for k in range(prefill + W, S):
+        if regen:
+            refill(k + K)  # fresh steps (a repeated pair would take the rejection path)
         step(k)
     torch.cuda.synchronize()
     prof = ig_profile_read(hp.h)
@@ -358,35 +412,45 @@ def run_ours(args, world, rank, local):
                 "step_frac": (step_bytes / (ms_per_step * 1e-3) / 1e9) / peak}
 
     # ---- end to end through the public host-buffer API (H2D of inputs and D2H of guesses timed)
-    P = min(4, K)
-    host = [tuple(t.cpu().pin_memory() for t in pool[prefill + W + j]) for j in range(P)]
-    x0h_p = torch.zeros(N, dtype=torch.float64).pin_memory()
-    x0h_e = torch.zeros(N, dtype=torch.float64).pin_memory()
-    KE = max(1, args.e2e_steps)
-    barrier(world)
-    torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    for j in range(KE):
-        b, x, Ax = host[j % P]
+    # M+1 distinct host steps: a pair re-enters only after it left the M-window (admission path)
+    PH = M + 1
+    if regen or PH > len(pool) or 3 * PH * vec_gb > 32.0:
+        e2e = {"value": None, "unit": "GB/s", "h2d_bytes_per_step": 4 * 8 * N, "d2h_bytes_per_step": 2 * 8 * N,
+               "unavailable": "M+1 distinct pinned host input steps (to stay on the admission path) exceed 32 GB"}
+    else:
+        host = [tuple(t.cpu().pin_memory() for t in pool[(prefill + W + j) % len(pool)]) for j in range(PH)]
+        x0h_p = torch.zeros(N, dtype=torch.float64).pin_memory()
+        x0h_e = torch.zeros(N, dtype=torch.float64).pin_memory()
+        KE = max(1, args.e2e_steps)
+        # one untimed call pair per handle: allocates the staging buffers outside the timed region
+        b, x, Ax = host[PH - 1]
         ig_form_guess_host(hp.h, b, x0h_p)
-        ig_update_host(hp.h, x, Ax)
         ig_form_guess_host(he.h, None, x0h_e)
-        ig_update_host(he.h, x, None)
-    torch.cuda.synchronize()
-    te = max_over_ranks(time.perf_counter() - t0, world)
-    e2e = {"value": world * step_bytes * KE / te / 1e9, "unit": "GB/s", "ms_per_step": te / KE * 1e3,
-           "h2d_bytes_per_step": 4 * 8 * N, "d2h_bytes_per_step": 2 * 8 * N, "steps": KE,
-           "h2d_vectors": "QR: b, x, Ax (the fallback x0 is not uploaded once d > 0); EXTRAP: x",
-           "api": "ig_form_guess_host/ig_update_host (pinned host buffers)"}
+        barrier(world)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for j in range(KE):
+            b, x, Ax = host[j % PH]
+            ig_form_guess_host(hp.h, b, x0h_p)
+            ig_update_host(hp.h, x, Ax)
+            ig_form_guess_host(he.h, None, x0h_e)
+            ig_update_host(he.h, x, None)
+        torch.cuda.synchronize()
+        te = max_over_ranks(time.perf_counter() - t0, world)
+        e2e = {"value": world * step_bytes * KE / te / 1e9, "unit": "GB/s", "ms_per_step": te / KE * 1e3,
+               "h2d_bytes_per_step": 4 * 8 * N, "d2h_bytes_per_step": 2 * 8 * N, "steps": KE,
+               "h2d_vectors": "QR: b, x, Ax (the fallback x0 is not uploaded once d > 0); EXTRAP: x",
+               "api": "ig_form_guess_host/ig_update_host (pinned host buffers)"}
 
     # ---- CPU oracle baseline (rank 0, N=1 only)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        sps, bps, done, Ns = oracle_sample_run(n, M, p, n, 10 ** 6, args.cpu_seconds, M + 1)
+        nz_cpu = n if N <= (1 << 22) else max(1, (1 << 21) // (n * n))  # big configs: a 2M-DOF z-slab sample
+        sps, bps, done, Ns = oracle_sample_run(n, M, p, nz_cpu, 10 ** 6, args.cpu_seconds, M + 1)
         cpu = {"value": bps / sps / 1e9, "unit": "GB/s", "cores": cpu_cores(), "kind": "oracle",
                "ms_per_step": sps * 1e3,
-               "sample": f"full {n}^3 grid ({Ns} DOFs), {done} steady oracle steps (QR({M})+EXTRAP({p},{M})) "
-                         f"after {M + 1} fill steps, ~{args.cpu_seconds:.0f} s budget"}
+               "sample": f"{Ns} DOFs ({'full grid' if Ns == N else 'z-slab sample'}), {done} steady oracle steps "
+                         f"(QR({M})+EXTRAP({p},{M})) after {M + 1} fill steps, ~{args.cpu_seconds:.0f} s budget"}
 
     hp.close()
     he.close()
@@ -394,13 +458,16 @@ def run_ours(args, world, rank, local):
         out = {"metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": K, "warmup": W,
                "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
                "dtype": "f64", "data": "synthetic",
-               "config": {"workload": f"C2 3D {n}^3 7-point Helmholtz manufactured sequence, QR({M}) + EXTRAP({p},{M})",
-                          "dofs_per_gpu": N, "history_m": M, "degree": p, "prefill_steps": prefill,
+               "config": {"workload": f"{args.cfg_name}: 3D {n}x{n}x{nz} 7-point Helmholtz manufactured sequence "
+                                      f"per GPU, QR({M}) + EXTRAP({p},{M})",
+                          "dofs_per_gpu": N, "input_pool_steps": P,
+                          "timing": ("K per-step event windows summed; inputs regenerated between steps outside "
+                                     "the windows (history + inputs exceed HBM)") if regen else "one event window over K steps", "history_m": M, "degree": p, "prefill_steps": prefill,
                           "bytes_per_step_per_gpu": step_bytes,
                           "bytes_model": "QR (8M+4)*8N + EXTRAP (nnz(beta)+1)*8N + push copy 2*8N",
                           "extrap_nnz": nnz,
-                          "l2": f"fresh inputs every step; per-step working set "
-                                f"{(2 * M + M + 5) * 8 * N / 1e9:.2f} GB > L2 126 MB",
+                          "l2": (f"fresh inputs every step" if P == S else f"inputs cycled over {P} steps")
+                                + f"; per-step working set {(2 * M + M + 5) * 8 * N / 1e9:.2f} GB > L2 126 MB",
                           "parallelism": f"dof-shard{world}" if world > 1 else "single",
                           "exchange": (args.exchange if world > 1 else "none"),
                           "mode": "TEST: all ranks on one GPU" if args.same_gpu else "one rank per GPU"},
