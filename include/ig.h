@@ -89,10 +89,15 @@ int ig_set_stream(ig_t h, void *cuda_stream);
  * admitted iff ||b~|| > eps_rel * ||A x|| after the two Gram-Schmidt passes.  Default 1e-10. */
 int ig_set_admit_tol(ig_t h, double eps_rel);
 
-/* Projection kernel schedule.  fused = 1 (default): on a single rank each ig_form_guess /
- * ig_update is ONE persistent cooperatively-launched kernel whose passes are separated by
- * software grid barriers.  fused = 0, or any handle with an attached multi-rank communicator:
- * one kernel per pass with the NCCL exchange of partial sums between them.  Same arithmetic. */
+/* Projection kernel schedule.  fused = 1 (default): on a single rank (or with the in-kernel peer
+ * exchange, ig_attach_peers) each ig_form_guess / ig_update is ONE persistent kernel whose passes
+ * are separated by software grid barriers.  Its grid (SMs x occupancy, or ig_set_grid_limit) must
+ * be resident at once: by default it is launched as an ordinary kernel (faster, PDL-chained),
+ * which assumes no kernel on another stream holds SMs until this one finishes; env
+ * IG_LAUNCH=coop,pdl makes the driver guarantee co-residency (cooperative launch).  A barrier
+ * that cannot complete gives up after the watchdog time (ig_set_watchdog) and reports
+ * IG_E_STATE.  fused = 0, or a handle with an NCCL communicator (ig_attach_comm): one kernel per
+ * pass with the NCCL exchange of partial sums between them.  Same arithmetic. */
 int ig_set_schedule(ig_t h, int fused);
 
 /* ---------------------------------------------------------------- the hot path */

@@ -144,7 +144,7 @@ cudaError_t launch_form_combine(const ProjArgs &a, int vec, int nsm, cudaStream_
 cudaError_t launch_u1(const ProjArgs &a, int vec, int nsm, cudaStream_t s);
 cudaError_t launch_u2(const ProjArgs &a, int vec, int nsm, cudaStream_t s);
 cudaError_t launch_u3(const ProjArgs &a, int vec, int nsm, cudaStream_t s);
-// Persistent fused kernels (single GPU): one cooperative launch per call.
+// Persistent fused kernels (single GPU / peer exchange): one launch per call (see launch policy).
 cudaError_t launch_form_fused(const ProjArgs &a, int vec, int nsm, cudaStream_t s);
 cudaError_t launch_update_fused(const ProjArgs &a, int vec, int nsm, cudaStream_t s);
 cudaError_t launch_extrap(const ExtrapArgs &a, int vec, int nsm, cudaStream_t s);

@@ -1,4 +1,5 @@
-// kern_fused.cu -- persistent, cooperatively launched projection kernels for a single GPU.
+// kern_fused.cu -- persistent projection kernels (one launch per call) for a single GPU and for
+// the in-kernel peer exchange; launched as ordinary PDL-chained kernels by default (IG_LAUNCH).
 //
 // One launch per library call instead of one per pass: the passes of Alg. 2
 // are separated by software grid barriers, and after each reduction EVERY CTA sums the block
@@ -305,7 +306,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_update_fused(ProjArgs a) {
     if (a.method == M_PROJ_QR && dnew == M && threadIdx.x < 32) givens_plan(c, M, s_H);
 }
 
-// ------------------------------------------------------------------ cooperative launchers
+// ------------------------------------------------------------------ launchers (cooperative iff IG_LAUNCH has "coop")
 template <class K> static cudaError_t coop_launch(K kern, const ProjArgs &a, int nsm, cudaStream_t s) {
     static_assert(sizeof(ProjArgs) < 4096, "kernel parameters");
     int occ = cached_occupancy((const void *)kern);
