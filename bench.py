@@ -32,6 +32,7 @@ sys.path.insert(0, ROOT)
 
 METRIC = "initial-guess form+update time/step & effective HBM GB/s (% of roofline), 1/2/4/8 B200"
 FALLBACK_HBM = 6650.0  # B200_PROFILING.md fallback (GB/s)
+NOMINAL_HBM = 7700.0  # B200_PROFILING.md nominal HBM3e (HGX), for context
 L2_BYTES = 126 * 2 ** 20
 
 
@@ -50,6 +51,7 @@ def parse():
     p.add_argument("--e2e-steps", type=int, default=20)
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-seconds", type=float, default=15.0, help="budget of the oracle cpu_baseline sample")
+    p.add_argument("--cpu-seconds-1t", type=float, default=6.0, help="budget of the one-core oracle sample")
     p.add_argument("--same-gpu", action="store_true",
                    help="TEST MODE: all ranks on GPU 0 (gloo plumbing, 1/N of the SMs each) to exercise the N>1 path")
     p.add_argument("--exchange", choices=["peer", "nccl"], default="peer",
@@ -74,6 +76,29 @@ def peak_hbm():
             return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy read+write)"
     except Exception:
         return FALLBACK_HBM, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def read_only_ceiling(dev):
+    """In-run read-only HBM ceiling: dots are pure reads and can exceed the copy
+    rate.  torch.sum over a 2.1 GB fp64 vector, best of 5 (a measuring stick, not the product)."""
+    import torch
+
+    try:
+        t = torch.ones(1 << 28, dtype=torch.float64, device=dev)
+    except RuntimeError:
+        return None
+    best = None
+    for _ in range(6):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        t.sum()
+        b.record()
+        torch.cuda.synchronize()
+        ms = a.elapsed_time(b)
+        best = ms if best is None else min(best, ms)
+    del t
+    torch.cuda.empty_cache()
+    return 8 * (1 << 28) / (best * 1e-3) / 1e9
 
 
 def bytes_per_step(M: int, N: int, nnz: int | None = None):
@@ -287,6 +312,7 @@ def run_ours(args, world, rank, local):
         # fits.  Inputs are regenerated into fixed buffers between steps, OUTSIDE the timed
         # windows: every step is bracketed by its own events and the K windows are summed.
         P, regen = 1, True
+    ro_gbs = read_only_ceiling(dev) if rank == 0 else None
     pool = [manufactured_step_slab(n, nz, rank, world, k, device=dev) for k in range(P)]
     torch.cuda.synchronize()
 
@@ -344,7 +370,7 @@ def run_ours(args, world, rank, local):
             torch.cuda.synchronize()
             t_local = e0.elapsed_time(e1)
         else:
-            t_local, host_us, launches_regen = 0.0, 0.0, 0
+            t_local, host_us, launches_regen, step_ms = 0.0, 0.0, 0, []
             for k in range(prefill + W, S):
                 refill(k)
                 barrier(world)
@@ -355,7 +381,8 @@ def run_ours(args, world, rank, local):
                 e1.record(stream)
                 torch.cuda.synchronize()
                 launches_regen += ig_total_launches() - l1
-                t_local += e0.elapsed_time(e1)
+                step_ms.append(e0.elapsed_time(e1))
+                t_local += step_ms[-1]
     barrier(world)
     launches = ig_total_launches() - l0 if not regen else launches_regen
     t_ms = max_over_ranks(t_local, world)
@@ -409,7 +436,25 @@ def run_ours(args, world, rank, local):
     roofline = {"bound": "hbm", "kernel": f"k_{dom}", "achieved": kernels[dom]["gbs"], "peak": peak, "unit": "GB/s",
                 "frac": kernels[dom]["gbs"] / peak, "traffic": traffic, "peak_source": peak_src,
                 "algorithmic_bytes_per_launch": per_kernel[dom], "traffic_source": traffic_src,
-                "step_frac": (step_bytes / (ms_per_step * 1e-3) / 1e9) / peak}
+                "step_frac": (step_bytes / (ms_per_step * 1e-3) / 1e9) / peak,
+                "frac_nominal": kernels[dom]["gbs"] / NOMINAL_HBM,
+                "ceilings_gbs": {"copy_measured": peak, "read_only_measured": ro_gbs, "nominal": NOMINAL_HBM,
+                                 "read_only_how": "torch.sum over 2^28 fp64 (2.1 GB), best of 5, CUDA events"}}
+
+    # ---- per-step distribution: a third pass with an event between consecutive steps (regen
+    # mode: the headline's own per-step windows)
+    if not regen:
+        evs = [torch.cuda.Event(enable_timing=True) for _ in range(K + 1)]
+        evs[0].record(stream)
+        for j, k in enumerate(range(prefill + W, S)):
+            step(k)
+            evs[j + 1].record(stream)
+        torch.cuda.synchronize()
+        step_ms = [evs[j].elapsed_time(evs[j + 1]) for j in range(K)]
+    q = statistics.quantiles(step_ms, n=10) if len(step_ms) >= 2 else [step_ms[0]] * 9
+    step_stats = {"median_us": statistics.median(step_ms) * 1e3, "p10_us": q[0] * 1e3, "p90_us": q[-1] * 1e3,
+                  "steps": len(step_ms), "how": "per-step CUDA events (separate pass)" if not regen
+                  else "the headline's per-step windows"}
 
     # ---- end to end through the public host-buffer API (H2D of inputs and D2H of guesses timed)
     # M+1 distinct host steps: a pair re-enters only after it left the M-window (admission path)
@@ -442,12 +487,37 @@ def run_ours(args, world, rank, local):
                "h2d_vectors": "QR: b, x, Ax (the fallback x0 is not uploaded once d > 0); EXTRAP: x",
                "api": "ig_form_guess_host/ig_update_host (pinned host buffers)"}
 
+    # ---- fill phase (reported separately from the steady state): both histories
+    # reset, the first M+1 steps timed one by one (projection d = 0..M, extrapolation fill 0..M)
+    fill = None
+    if not regen:
+        hp.reset()
+        he.reset()
+        torch.cuda.synchronize()
+        f_us, f_bytes = [], []
+        for j in range(M + 1):
+            e0.record(stream)
+            step(prefill + W + j)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            f_us.append(e0.elapsed_time(e1) * 1e3)
+            (a, b_), (c, d_) = hp.bytes(), he.bytes()
+            f_bytes.append(a + b_ + c + d_)
+        fill = {"steps": M + 1, "us_per_step": [round(v, 1) for v in f_us],
+                "gbs_per_step": [round(bb / (u * 1e-6) / 1e9) for bb, u in zip(f_bytes, f_us)],
+                "bytes_per_step": f_bytes, "total_us": sum(f_us)}
+
     # ---- CPU oracle baseline (rank 0, N=1 only)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         nz_cpu = n if N <= (1 << 22) else max(1, (1 << 21) // (n * n))  # big configs: a 2M-DOF z-slab sample
         sps, bps, done, Ns = oracle_sample_run(n, M, p, nz_cpu, 10 ** 6, args.cpu_seconds, M + 1)
+        from threadpoolctl import threadpool_limits
+
+        with threadpool_limits(limits=1):  # the same oracle on one host core
+            sps1, bps1, done1, _ = oracle_sample_run(n, M, p, nz_cpu, 10 ** 6, args.cpu_seconds_1t, M + 1)
         cpu = {"value": bps / sps / 1e9, "unit": "GB/s", "cores": cpu_cores(), "kind": "oracle",
+               "one_core": {"value": bps1 / sps1 / 1e9, "unit": "GB/s", "cores": 1, "steps": done1},
                "ms_per_step": sps * 1e3,
                "sample": f"{Ns} DOFs ({'full grid' if Ns == N else 'z-slab sample'}), {done} steady oracle steps "
                          f"(QR({M})+EXTRAP({p},{M})) after {M + 1} fill steps, ~{args.cpu_seconds:.0f} s budget"}
@@ -471,7 +541,8 @@ def run_ours(args, world, rank, local):
                           "parallelism": f"dof-shard{world}" if world > 1 else "single",
                           "exchange": (args.exchange if world > 1 else "none"),
                           "mode": "TEST: all ranks on one GPU" if args.same_gpu else "one rank per GPU"},
-               "gpu_launches": launches, "roofline": roofline, "kernels": kernels,
+               "gpu_launches": launches, "roofline": roofline, "kernels": kernels, "step_stats": step_stats,
+               "fill_phase": fill,
                "clocks": sampler.summary(), "e2e": e2e, "cpu_baseline": cpu,
                "proj_state": {"d": st["d"], "rho_last": st["rho"]}, "host_enqueue_us_per_step": host_us}
         print(json.dumps(out), flush=True)
