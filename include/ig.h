@@ -135,6 +135,15 @@ int ig_update_batch(int n, ig_t *handles, const double *const *xs, const double 
 int ig_form_guess_host(ig_t h, const double *b, double *x0);
 int ig_update_host(ig_t h, const double *x, const double *Ax);
 
+/* Host-buffer batch (several fields of one time step; arguments as in
+ * ig_form_guess_batch / ig_update_batch, but host arrays; pinned memory gives the overlap):
+ * one synchronisation per call, and the transfers of different fields overlap each other and the
+ * kernels -- the extrapolation guesses travel device->host while the projection right-hand sides
+ * travel host->device; the extrapolation uploads run while the projection update kernels run.
+ * Each handle gets a second (copy) stream on first use.  Same results as the single calls. */
+int ig_form_guess_batch_host(int n, ig_t *handles, const double *const *bs, double *const *x0s);
+int ig_update_batch_host(int n, ig_t *handles, const double *const *xs, const double *const *Axs);
+
 /* Extrapolation zero-copy slot: the device vector the next ig_update(h, slot, NULL) will push
  * without a copy.  The caller may solve directly into it (it may also be the x0 of
  * ig_form_guess).  NULL for projection methods. */

@@ -45,6 +45,8 @@ _SIGS = {
     "ig_form_guess_batch": (C.c_int, [C.c_int, C.POINTER(_P), C.POINTER(_P), C.POINTER(_P)]),
     "ig_update_batch": (C.c_int, [C.c_int, C.POINTER(_P), C.POINTER(_P), C.POINTER(_P)]),
     "ig_update_host": (C.c_int, [_P, _P, _P]),
+    "ig_form_guess_batch_host": (C.c_int, [C.c_int, C.POINTER(_P), C.POINTER(_P), C.POINTER(_P)]),
+    "ig_update_batch_host": (C.c_int, [C.c_int, C.POINTER(_P), C.POINTER(_P), C.POINTER(_P)]),
     "ig_next_slot": (_P, [_P]),
     "ig_comm_unique_id": (C.c_int, [_P]),
     "ig_comm_create": (C.c_int, [C.c_int, C.c_int, _P, C.POINTER(_P)]),

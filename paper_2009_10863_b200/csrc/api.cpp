@@ -152,6 +152,9 @@ struct ig_ctx {
     // host staging (end-to-end path)
     double *stage[4] = {nullptr, nullptr, nullptr, nullptr};
     int known_d = 0;  // projection d as of the last synchronising host-buffer call (-1: unknown)
+    cudaStream_t cstream = nullptr;  // batch host calls: copies that overlap the handle's stream
+    cudaEvent_t cev[2] = {nullptr, nullptr};
+    int *pin_ctrl = nullptr;         // pinned copy of the control block's leading ints (d ... err)
     int64_t launches = 0;
     // per-kernel CUDA-event timing (ig_profile)
     bool profiling = false;
@@ -388,6 +391,10 @@ void ig_destroy(ig_t h) {
     if (h->gath != h->part) cudaFree(h->gath);
     cudaFree(h->part);
     for (auto &s : h->stage) cudaFree(s);
+    for (auto e : h->cev)
+        if (e) cudaEventDestroy(e);
+    if (h->cstream) cudaStreamDestroy(h->cstream);
+    if (h->pin_ctrl) cudaFreeHost(h->pin_ctrl);
     for (void *p : h->ipc_opened) cudaIpcCloseMemHandle(p);
     cudaFree(h->xwin);
     prof_drain(h);
@@ -548,6 +555,7 @@ int ig_update(ig_t h, const double *x, const double *Ax) {
         ProjArgs a = proj_args(h);
         a.x = x;
         a.Ax = Ax;
+        h->known_d = -1;  // d is decided on the device
         const int vec = (al16(x) && al16(Ax)) ? 2 : 1;
         if (use_fused(h)) {
             Prof p(h, IG_K_UPDATE_FUSED);
@@ -633,12 +641,45 @@ int ig_update_batch(int n, ig_t *hs, const double *const *xs, const double *cons
     return IG_OK;
 }
 
+static int watchdog_error(int err);
+
 static int ensure_stage(ig_t h) {
     for (auto &s : h->stage)
         if (!s && cudaMalloc(&s, sizeof(double) * (size_t)h->ld) != cudaSuccess) {
             cudaGetLastError();
             return set_err(IG_E_OOM, "staging buffer allocation failed");
         }
+    if (is_proj(h->method) && !h->pin_ctrl && cudaMallocHost(&h->pin_ctrl, offsetof(Ctrl, ticket)) != cudaSuccess) {
+        cudaGetLastError();
+        return set_err(IG_E_OOM, "pinned control readback allocation failed");
+    }
+    return IG_OK;
+}
+
+// Second stream + events for the batch host calls (copies overlapping the handle's stream).
+static int ensure_cstream(ig_t h) {
+    if (h->cstream) return IG_OK;
+    CUDA_OK(cudaStreamCreateWithFlags(&h->cstream, cudaStreamNonBlocking));
+    for (auto &e : h->cev) CUDA_OK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    return IG_OK;
+}
+
+// Projection: the update's d / watchdog flag travel back with the call's own synchronisation
+// (4 x int32 D2H enqueued after the kernel), so the next ig_form_guess_host knows whether the
+// fallback x0 is needed (d == 0) without another stream round trip.
+static int ctrl_readback(ig_t h) { CUDA_OK(cudaMemcpyAsync(h->pin_ctrl, h->ctrl, offsetof(Ctrl, ticket), cudaMemcpyDeviceToHost, h->stream)); return IG_OK; }
+static int ctrl_consume(ig_t h) {
+    Ctrl c;
+    memcpy(&c, h->pin_ctrl, offsetof(Ctrl, ticket));
+    h->known_d = c.d;
+    return watchdog_error(c.err);
+}
+static int known_dim(ig_t h) {
+    if (h->known_d >= 0) return IG_OK;
+    int d = 0;
+    int rc = ig_history_dim(h, &d);
+    if (rc) return rc;
+    h->known_d = d;
     return IG_OK;
 }
 
@@ -650,23 +691,11 @@ int ig_form_guess_host(ig_t h, const double *b, double *x0) {
     const size_t nb = sizeof(double) * (size_t)h->N;
     if (is_proj(h->method)) {
         if (!b) return set_err(IG_E_ARG, "b is NULL");
+        rc = known_dim(h);
+        if (rc) return rc;
         CUDA_OK(cudaMemcpyAsync(h->stage[0], b, nb, cudaMemcpyHostToDevice, h->stream));
         // the fallback x0 is only read when d == 0: skip its upload otherwise
-        if (h->known_d != 0) {
-            int d = 0;
-            rc = ig_history_dim(h, &d);
-            if (rc) return rc;
-            h->known_d = d;
-        }
-        if (h->known_d == 0) {
-            CUDA_OK(cudaMemcpyAsync(h->stage[1], x0, nb, cudaMemcpyHostToDevice, h->stream));
-        } else {
-            rc = ig_form_guess(h, h->stage[0], h->stage[1]);
-            if (rc) return rc;
-            CUDA_OK(cudaMemcpyAsync(x0, h->stage[1], nb, cudaMemcpyDeviceToHost, h->stream));
-            CUDA_OK(cudaStreamSynchronize(h->stream));
-            return IG_OK;
-        }
+        if (h->known_d == 0) CUDA_OK(cudaMemcpyAsync(h->stage[1], x0, nb, cudaMemcpyHostToDevice, h->stream));
         rc = ig_form_guess(h, h->stage[0], h->stage[1]);
         if (rc) return rc;
     } else {
@@ -691,15 +720,118 @@ int ig_update_host(ig_t h, const double *x, const double *Ax) {
         CUDA_OK(cudaMemcpyAsync(h->stage[3], Ax, nb, cudaMemcpyHostToDevice, h->stream));
         rc = ig_update(h, h->stage[2], h->stage[3]);
         if (rc) return rc;
-        h->known_d = -1;  // re-read (4 bytes) by the next ig_form_guess_host
-    } else {
-        double *slot = next_slot_ptr(h);  // copy straight into the ring slot: zero-copy push
-        CUDA_OK(cudaMemcpyAsync(slot, x, nb, cudaMemcpyHostToDevice, h->stream));
-        int rc = ig_update(h, slot, nullptr);
+        rc = ctrl_readback(h);
         if (rc) return rc;
+        CUDA_OK(cudaStreamSynchronize(h->stream));
+        return ctrl_consume(h);
     }
+    double *slot = next_slot_ptr(h);  // copy straight into the ring slot: zero-copy push
+    CUDA_OK(cudaMemcpyAsync(slot, x, nb, cudaMemcpyHostToDevice, h->stream));
+    int rc = ig_update(h, slot, nullptr);
+    if (rc) return rc;
     CUDA_OK(cudaStreamSynchronize(h->stream));
     return IG_OK;
+}
+
+// Batch host calls (several fields, one synchronisation): the PCIe transfers of different fields
+// overlap each other and the kernels (pinned host memory; H2D and D2H run on separate engines).
+int ig_form_guess_batch_host(int n, ig_t *hs, const double *const *bs, double *const *x0s) {
+    if (n < 0 || (n > 0 && (!hs || !x0s))) return set_err(IG_E_ARG, "bad batch arguments");
+    for (int i = 0; i < n; ++i) {
+        if (!hs[i] || !x0s[i]) return set_err(IG_E_ARG, "NULL handle or x0 in batch");
+        if (is_proj(hs[i]->method) && (!bs || !bs[i])) return set_err(IG_E_ARG, "b is NULL");
+        DevGuard g(hs[i]->dev);
+        int rc = ensure_stage(hs[i]);
+        if (!rc) rc = ensure_cstream(hs[i]);
+        if (!rc && is_proj(hs[i]->method)) rc = known_dim(hs[i]);
+        if (rc) return rc;
+    }
+    // 1) extrapolation fields first (no inputs): kernel on the handle's stream, D2H of the guess on
+    //    the handle's copy stream, so it overlaps the projection fields' H2D of b
+    for (int i = 0; i < n; ++i) {
+        ig_t q = hs[i];
+        if (!is_extrap(q->method) || q->fill == 0) continue;  // fill == 0: x0 untouched
+        DevGuard g(q->dev);
+        int rc = ig_form_guess(q, nullptr, q->stage[1]);
+        if (rc) return rc;
+        CUDA_OK(cudaEventRecord(q->cev[0], q->stream));
+        CUDA_OK(cudaStreamWaitEvent(q->cstream, q->cev[0], 0));
+        CUDA_OK(cudaMemcpyAsync(x0s[i], q->stage[1], sizeof(double) * (size_t)q->N, cudaMemcpyDeviceToHost,
+                                q->cstream));
+    }
+    // 2) projection fields: H2D b (and the fallback x0 iff d == 0), kernel, D2H of the guess
+    for (int i = 0; i < n; ++i) {
+        ig_t h = hs[i];
+        if (!is_proj(h->method)) continue;
+        DevGuard g(h->dev);
+        const size_t nb = sizeof(double) * (size_t)h->N;
+        CUDA_OK(cudaMemcpyAsync(h->stage[0], bs[i], nb, cudaMemcpyHostToDevice, h->stream));
+        if (h->known_d == 0) CUDA_OK(cudaMemcpyAsync(h->stage[1], x0s[i], nb, cudaMemcpyHostToDevice, h->stream));
+        int rc = ig_form_guess(h, h->stage[0], h->stage[1]);
+        if (rc) return rc;
+        CUDA_OK(cudaMemcpyAsync(x0s[i], h->stage[1], nb, cudaMemcpyDeviceToHost, h->stream));
+    }
+    for (int i = 0; i < n; ++i) {
+        DevGuard g(hs[i]->dev);
+        CUDA_OK(cudaStreamSynchronize(hs[i]->stream));
+        CUDA_OK(cudaStreamSynchronize(hs[i]->cstream));
+    }
+    return IG_OK;
+}
+
+int ig_update_batch_host(int n, ig_t *hs, const double *const *xs, const double *const *Axs) {
+    if (n < 0 || (n > 0 && (!hs || !xs))) return set_err(IG_E_ARG, "bad batch arguments");
+    for (int i = 0; i < n; ++i) {
+        if (!hs[i] || !xs[i]) return set_err(IG_E_ARG, "NULL handle or x in batch");
+        if (is_proj(hs[i]->method) && (!Axs || !Axs[i])) return set_err(IG_E_ARG, "Ax is NULL");
+        DevGuard g(hs[i]->dev);
+        int rc = ensure_stage(hs[i]);
+        if (!rc) rc = ensure_cstream(hs[i]);
+        if (rc) return rc;
+    }
+    // 1) projection fields: H2D x, Ax, then the update kernel
+    ig_t last_proj = nullptr;
+    for (int i = 0; i < n; ++i) {
+        ig_t h = hs[i];
+        if (!is_proj(h->method)) continue;
+        DevGuard g(h->dev);
+        const size_t nb = sizeof(double) * (size_t)h->N;
+        CUDA_OK(cudaMemcpyAsync(h->stage[2], xs[i], nb, cudaMemcpyHostToDevice, h->stream));
+        CUDA_OK(cudaMemcpyAsync(h->stage[3], Axs[i], nb, cudaMemcpyHostToDevice, h->stream));
+        CUDA_OK(cudaEventRecord(h->cev[1], h->stream));  // uploads done (the kernel follows)
+        int rc = ig_update(h, h->stage[2], h->stage[3]);
+        if (!rc) rc = ctrl_readback(h);
+        if (rc) return rc;
+        last_proj = h;
+    }
+    // 2) extrapolation fields: H2D of x straight into the ring slot on the copy stream, after the
+    //    projection uploads (PCIe is shared) so it overlaps the projection update kernels; the
+    //    handle's stream then waits for it (later kernels read the slot)
+    for (int i = 0; i < n; ++i) {
+        ig_t q = hs[i];
+        if (!is_extrap(q->method)) continue;
+        DevGuard g(q->dev);
+        double *slot = next_slot_ptr(q);
+        CUDA_OK(cudaEventRecord(q->cev[0], q->stream));  // readers of the slot's old solution
+        CUDA_OK(cudaStreamWaitEvent(q->cstream, q->cev[0], 0));
+        if (last_proj && last_proj->dev == q->dev) CUDA_OK(cudaStreamWaitEvent(q->cstream, last_proj->cev[1], 0));
+        CUDA_OK(cudaMemcpyAsync(slot, xs[i], sizeof(double) * (size_t)q->N, cudaMemcpyHostToDevice, q->cstream));
+        CUDA_OK(cudaEventRecord(q->cev[1], q->cstream));
+        CUDA_OK(cudaStreamWaitEvent(q->stream, q->cev[1], 0));
+        int rc = ig_update(q, slot, nullptr);  // zero-copy push
+        if (rc) return rc;
+    }
+    int first_err = IG_OK;
+    for (int i = 0; i < n; ++i) {
+        DevGuard g(hs[i]->dev);
+        CUDA_OK(cudaStreamSynchronize(hs[i]->stream));
+        CUDA_OK(cudaStreamSynchronize(hs[i]->cstream));
+        if (is_proj(hs[i]->method)) {
+            int rc = ctrl_consume(hs[i]);
+            if (rc && !first_err) first_err = rc;
+        }
+    }
+    return first_err;
 }
 
 double *ig_next_slot(ig_t h) {

@@ -137,6 +137,23 @@ def ig_update_batch(handles, xs, Axs=None) -> None:
     _check(lib().ig_update_batch(n, hb, xp, ap), "ig_update_batch")
 
 
+def ig_form_guess_batch_host(handles, bs, x0s) -> None:
+    """Host-buffer batch guess (include/ig.h): transfers of the fields overlap; syncs once."""
+    n = len(handles)
+    hb = _ptr_array([h.h if isinstance(h, InitialGuess) else h for h in handles])
+    bp = _ptr_array([_hptr(b, "b") for b in bs]) if bs is not None else None
+    xp = _ptr_array([_hptr(x, "x0") for x in x0s])
+    _check(lib().ig_form_guess_batch_host(n, hb, bp, xp), "ig_form_guess_batch_host")
+
+
+def ig_update_batch_host(handles, xs, Axs=None) -> None:
+    n = len(handles)
+    hb = _ptr_array([h.h if isinstance(h, InitialGuess) else h for h in handles])
+    xp = _ptr_array([_hptr(x, "x") for x in xs])
+    ap = _ptr_array([_hptr(a, "Ax") for a in Axs]) if Axs is not None else None
+    _check(lib().ig_update_batch_host(n, hb, xp, ap), "ig_update_batch_host")
+
+
 def ig_form_guess_host(h, b, x0) -> None:
     _check(lib().ig_form_guess_host(h, _hptr(b, "b"), _hptr(x0, "x0")), "ig_form_guess_host")
 

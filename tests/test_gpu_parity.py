@@ -272,6 +272,46 @@ def test_host_entry_points_match_oracle():
     he.close()
 
 
+def test_batch_host_entry_points_match_single_calls_and_oracle():
+    """ig_form_guess_batch_host / ig_update_batch_host (transfers of the fields overlapped on two
+    streams per handle) against the device-buffer single calls on twin handles, bitwise, and the
+    oracle within 1e-11 -- including the fill phase (d = 0: the fallback x0 must come back
+    unchanged), a restart of a CLASSIC field and a zero right-hand side."""
+    from paper_2009_10863_b200 import InitialGuess, ig_form_guess_batch_host, ig_update_batch_host
+
+    g = Grid(26, 2)
+    N = g.N
+    seq = _seq(g, 14, dt=1e-2)
+    specs = [("extrap_ls", 4, 2), ("proj_qr", 5, 0), ("extrap_sparse", 6, 1), ("proj_classic", 3, 0)]
+    A = [InitialGuess(N, m, M, p) for m, M, p in specs]
+    B = [InitialGuess(N, m, M, p) for m, M, p in specs]
+    oras = [ExtrapLS(N, 4, 2), ProjQR(N, 5), None, ProjClassic(N, 3)]
+    for n, (b, x, Ax) in enumerate(seq):
+        if n == 5:
+            b = np.zeros(N)  # zero right-hand side: projection guess 0
+        fb = np.full(N, -2.5)
+        x0h = [torch.from_numpy(fb.copy()).pin_memory() for _ in specs]
+        bh = [torch.from_numpy(b).pin_memory() if m.startswith("proj") else None for m, _, _ in specs]
+        ig_form_guess_batch_host(A, bh, x0h)
+        for i, ((m, _, _), h) in enumerate(zip(specs, B)):
+            x0d = torch.from_numpy(fb.copy()).cuda()
+            h.form_guess(torch.from_numpy(b).cuda() if m.startswith("proj") else None, x0d)
+            assert torch.equal(x0h[i], x0d.cpu()), (n, specs[i])
+            if oras[i] is not None:
+                assert _rel(x0h[i].numpy(), oras[i].form_guess(b, fb)) <= TOL, (n, specs[i])
+        xh = [torch.from_numpy(x).pin_memory() for _ in specs]
+        Axh = [torch.from_numpy(Ax).pin_memory() if m.startswith("proj") else None for m, _, _ in specs]
+        ig_update_batch_host(A, xh, Axh)
+        for (m, _, _), h, o in zip(specs, B, oras):
+            h.update(torch.from_numpy(x).cuda(), torch.from_numpy(Ax).cuda() if m.startswith("proj") else None)
+            if o is not None:
+                o.update(x, Ax)
+    for ha, hb in zip(A, B):
+        assert ha.save_state() == hb.save_state()
+        ha.close()
+        hb.close()
+
+
 # ------------------------------------------------------------------ full C2 size (bench launch config)
 @pytest.mark.slow
 def test_c2_full_size_parity():
