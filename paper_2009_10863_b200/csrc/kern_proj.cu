@@ -205,7 +205,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_u3(ProjArgs a) {
     __shared__ double s_nb, s_nAx;
     __shared__ int s_adm;
     __shared__ unsigned s_ticket;
-    __shared__ double s_H[MAXM * MAXM];
+    __shared__ double s_W[MAXM * 32];  // Givens-plan scratch (last block)
     Ctrl *c = a.ctrl;
     const int deff = c->deff, M = a.M;
     const bool rotX = c->rotX != 0;
@@ -286,7 +286,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_u3(ProjArgs a) {
         c->rotX = 0;
         c->ticket[ST_U3] = 0;
     }
-    if (a.method == M_PROJ_QR && dnew == M && threadIdx.x < 32) givens_plan(c, M, s_H);
+    if (a.method == M_PROJ_QR && dnew == M && threadIdx.x < 32) givens_plan(c, M, c->R, s_W);
 }
 
 // ------------------------------------------------------------------ launchers

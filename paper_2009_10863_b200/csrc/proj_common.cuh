@@ -564,34 +564,67 @@ __device__ __forceinline__ void u3trip_store(const U3Trip<MC, U, V> &r, const Pr
 
 // One warp: Givens parameters of the next downdate from R (AMB-2 reading of P:279-290):
 // H = R_{:,2:M}; for i: a = H_ii, b = H_{i+1,i}, r = hypot(a,b), c = a/r, s = b/r; rotate rows.
-static __device__ __noinline__ void givens_plan(Ctrl *c, int M, double *H) {
-    // Only the leading M x M block of R / Rdn is ever read: touch nothing else (this runs in
-    // the serial tail of the update kernel).  Lane j owns column j of H.
-    const int lane = threadIdx.x & 31, j = lane;
-    if (j < M - 1)
-        for (int i = 0; i < M; ++i) H[i * MAXM + j] = c->R[i + (j + 1) * MAXM];
+// Lane j owns column j of H (W[i*32 + j], shared scratch); `t` is its entry in the row carried
+// down (row i after rotations < i), b = H_{i+1,i} = R_{i+1,i+1}: one shuffle per rotation.  Row i
+// is final after rotation i and goes straight to Rdn.  Only the leading M x M block of R / Rdn
+// is touched.  The loops stay rolled on purpose: this runs once per call in a serial tail where
+// the code is cold in the instruction cache (an unrolled version measured 13 us cold vs 2.7 us
+// warm at M = 8), so code size, not instruction count, sets its time.
+static __device__ __noinline__ void givens_plan(Ctrl *c, int M, const double *R, double *W) {
+    const int j = threadIdx.x & 31;
+#pragma unroll 1
+    for (int i = 0; i < M; ++i) W[i * 32 + j] = (j < M - 1) ? R[i + (j + 1) * MAXM] : 0.0;  // H_ij = R_{i,j+1}
     __syncwarp();
+    double t = W[j], my_c = 1.0, my_s = 0.0;
+#pragma unroll 1
     for (int i = 0; i < M - 1; ++i) {
-        const double aa = H[i * MAXM + i], bb = H[(i + 1) * MAXM + i];
+        const double aa = __shfl_sync(0xffffffffu, t, i);
+        const double bb = R[(i + 1) + (i + 1) * MAXM];
         const double r = hypot(aa, bb);
         const double cs = (r == 0.0) ? 1.0 : aa / r;
         const double sn = (r == 0.0) ? 0.0 : bb / r;
-        __syncwarp();
+        if (j == i) {
+            my_c = cs;
+            my_s = sn;
+        }
         if (j >= i && j < M - 1) {
-            const double hi = H[i * MAXM + j], hi1 = H[(i + 1) * MAXM + j];
-            H[i * MAXM + j] = cs * hi + sn * hi1;
-            H[(i + 1) * MAXM + j] = -sn * hi + cs * hi1;
+            const double hi1 = W[(i + 1) * 32 + j];
+            c->Rdn[i + j * MAXM] = cs * t + sn * hi1;
+            t = -sn * t + cs * hi1;
         }
-        if (lane == 0) {
-            c->gc[i] = cs;
-            c->gs[i] = sn;
-        }
-        __syncwarp();
     }
-    if (j < M)  // column-major destination, leading M x M block
-        for (int i = 0; i < M; ++i) c->Rdn[i + j * MAXM] = (i < M - 1 && j < M - 1 && i <= j) ? H[i * MAXM + j] : 0.0;
+    if (j < M)  // the rest of the leading block of the downdated R is zero
+#pragma unroll 1
+        for (int i = 0; i < M; ++i)
+            if (!(i < M - 1 && j < M - 1 && i <= j)) c->Rdn[i + j * MAXM] = 0.0;
+    if (j < M - 1) {
+        c->gc[j] = my_c;
+        c->gs[j] = my_s;
+    }
     __syncwarp();
-    if (lane == 0) c->pending = 1;
+    if (j == 0) c->pending = 1;
+}
+
+// One warp: R after this update -- its leading M x M block is the downdated R (if a downdate ran)
+// plus, if the pair was admitted, the new column (c1 + c2; ||b~||) (Alg. 2) -- stored
+// to c->R and to sR (shared), then the Givens plan of the next downdate from sR.
+static __device__ __noinline__ void r_update_plan(Ctrl *c, int M, int deff, bool pend, bool newcol, bool plan,
+                                                  const double *r1, const double *r2, double nb, double *sR,
+                                                  double *sW) {
+    const int lane = threadIdx.x & 31;
+    const double *Rsrc = pend ? c->Rdn : c->R;
+#pragma unroll 1
+    for (int idx = lane; idx < M * M; idx += 32) {
+        const int i = idx % M, j = idx / M;
+        double v = Rsrc[i + j * MAXM];
+        if (newcol && j == deff) v = (i < deff) ? r1[i] + r2[i] : (i == deff ? nb : 0.0);
+        sR[i + j * MAXM] = v;
+        if (pend || (newcol && j == deff)) c->R[i + j * MAXM] = v;
+    }
+    if (newcol)
+        for (int k = M + lane; k < MAXM; k += 32) c->R[k + deff * MAXM] = 0.0;
+    __syncwarp();  // sR complete
+    if (plan) givens_plan(c, M, sR, sW);
 }
 
 }  // namespace ig
