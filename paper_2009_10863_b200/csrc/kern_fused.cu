@@ -20,13 +20,19 @@
 // Phase timestamps per CTA (debug builds with -DIG_TRACE=1; IG_TRACE_PTR = device buffer address
 // passed through the environment at launch): [cta][slot] = %globaltimer.
 #ifdef IG_TRACE
-__device__ unsigned long long g_trace[1024 * 12];
-#define TRACE(slot) do { if (threadIdx.x == 0) g_trace[blockIdx.x * 12 + (slot)] = globaltimer_ns(); } while (0)
+__device__ unsigned long long g_trace[1024 * 16];
+__device__ unsigned long long g_trace_form[1024 * 16];
+#define TRACE(slot) do { if (threadIdx.x == 0) g_trace[blockIdx.x * 16 + (slot)] = globaltimer_ns(); } while (0)
+#define TRACE_F(slot) do { if (threadIdx.x == 0) g_trace_form[blockIdx.x * 16 + (slot)] = globaltimer_ns(); } while (0)
 extern "C" int ig_debug_trace_read(unsigned long long *host, int n) {
     return (int)cudaMemcpyFromSymbol(host, g_trace, sizeof(unsigned long long) * n);
 }
+extern "C" int ig_debug_trace_read_form(unsigned long long *host, int n) {
+    return (int)cudaMemcpyFromSymbol(host, g_trace_form, sizeof(unsigned long long) * n);
+}
 #else
 #define TRACE(slot) do { } while (0)
+#define TRACE_F(slot) do { } while (0)
 #endif
 
 namespace ig {
@@ -41,7 +47,16 @@ __global__ void __launch_bounds__(THREADS, 1) k_form_fused(ProjArgs a) {
     constexpr int U = FusedUnroll<MC>::U;
     __shared__ double sh[(THREADS / 32) * (MC + 1)];
     __shared__ double s_red[PS];
+    TRACE_F(8);
     pdl_wait();  // stream predecessor complete and visible (programmatic dependent launch)
+    TRACE_F(0);
+#ifdef IG_TRACE
+    if (threadIdx.x == 0) {
+        unsigned sm;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+        g_trace_form[blockIdx.x * 16 + 12] = sm;
+    }
+#endif
     Ctrl *c = a.ctrl;
     const int d = c->d;
     if (d == 0) return;  // uniform: x0 stays the caller's fallback
@@ -81,8 +96,11 @@ __global__ void __launch_bounds__(THREADS, 1) k_form_fused(ProjArgs a) {
     XTrip<MC, U, V> pre;  // first trip of pass 2, in flight across the barrier
     xtrip_load(pre, a, i_first, stride, nv, d, ps);
     block_partials_store<MC + 1>(v, d, false, a.blk, sh);
+    TRACE_F(1);
     grid_barrier(&c->bar, 1, &c->err, a.watchdog_ns);
+    TRACE_F(2);
     reduce_all_blocks<MC>(d, false, a.blk, s_red);
+    TRACE_F(3);
     if (a.xc.G > 1) peer_allreduce(a.xc, ST_FORM, d, false, s_red, ep, &c->err, a.watchdog_ns);
     double al[MC];
 #pragma unroll
@@ -102,12 +120,15 @@ __global__ void __launch_bounds__(THREADS, 1) k_form_fused(ProjArgs a) {
             if (k < d) acc = fma(al[k], a.Xt[k * a.ld + i], acc);
         a.x0[i] = acc;
     }
+    TRACE_F(4);
     pdl_trigger();
     if (grid_exit(&c->bar, &c->bar_exit)) {
+        TRACE_F(9);
         if (threadIdx.x < d) a.part[ST_FORM * PS + threadIdx.x] = s_red[threadIdx.x];
         if (threadIdx.x < d && !isfinite(s_red[threadIdx.x])) watchdog_trip(&c->err, 3);
         if (threadIdx.x == 0 && a.xc.G > 1) c->xepoch[ST_FORM] = ep;
     }
+    TRACE_F(7);
 }
 
 template <int MC, int VEC>
@@ -124,6 +145,13 @@ __global__ void __launch_bounds__(THREADS, 1) k_update_fused(ProjArgs a) {
     __shared__ double s_R[MAXM * MAXM], s_W[MAXM * 32];
     TRACE(8);
     pdl_wait();  // stream predecessor complete and visible (programmatic dependent launch)
+#ifdef IG_TRACE
+    if (threadIdx.x == 0) {
+        unsigned sm;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+        g_trace[blockIdx.x * 16 + 12] = sm;
+    }
+#endif
     Ctrl *c = a.ctrl;
     const int d = c->d, M = a.M;
     const bool pend = c->pending != 0;

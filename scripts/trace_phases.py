@@ -1,4 +1,5 @@
-"""Per-phase timing of k_update_fused from a -DIG_TRACE=1 build (globaltimer stamps per CTA)."""
+"""Per-phase timing of k_update_fused and k_form_fused from a -DIG_TRACE=1 build (globaltimer
+stamps per CTA, SM id per CTA).  IG_TRACE=1 python -m paper_2009_10863_b200.build, then run this."""
 import ctypes as C, os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch
@@ -22,9 +23,9 @@ for k in range(14):  # the bench step: QR form, QR update (traced), EXTRAP form,
 torch.cuda.synchronize()
 L = lib()
 L.ig_debug_trace_read.argtypes = [C.c_void_p, C.c_int]
-buf = (C.c_ulonglong * (1024 * 12))()
-assert L.ig_debug_trace_read(buf, 1024 * 12) == 0
-raw = np.array(buf[:148 * 12], dtype=np.float64).reshape(148, 12)
+buf = (C.c_ulonglong * (1024 * 16))()
+assert L.ig_debug_trace_read(buf, 1024 * 16) == 0
+raw = np.array(buf[:148 * 16], dtype=np.float64).reshape(148, 16)
 t = raw[:, [8, 0, 1, 2, 3, 4, 5, 6, 7]]
 last = int(np.argmax(raw[:, 7]))  # the CTA that ran the epilogue
 t0 = t[:, 0].min()
@@ -37,3 +38,26 @@ e = (raw[last, [6, 9, 7]] - t0) / 1e3
 print(f"epilogue CTA {last}: pass3 done {e[0]:.1f}, after grid_exit {e[1]:.1f}, done {e[2]:.1f} us")
 pl = (raw[0, [10, 11]] - t0) / 1e3
 print(f"R update + Givens plan (CTA 0 warp 0, during pass 3): {pl[0]:.1f} -> {pl[1]:.1f} us ({pl[1] - pl[0]:.1f} us)")
+
+# ---- k_form_fused of the same (last) step
+L.ig_debug_trace_read_form.argtypes = [C.c_void_p, C.c_int]
+assert L.ig_debug_trace_read_form(buf, 1024 * 16) == 0
+rf = np.array(buf[:148 * 16], dtype=np.float64).reshape(148, 16)
+tf = (rf[:, [8, 0, 1, 2, 3, 4, 7]] - rf[:, 8].min()) / 1e3
+print("k_form_fused:")
+for j, nm in enumerate(["CTA begin", "pdl_wait out", "pass1 done", "barrier out", "reduce done", "pass2 done", "exit"]):
+    print(f"  {nm:14s} min {tf[:, j].min():8.1f} med {np.median(tf[:, j]):8.1f} max {tf[:, j].max():8.1f} us")
+lf = int(np.argmax(rf[:, 7]))
+print(f"  last CTA {lf}: after grid_exit {(rf[lf, 9] - rf[:, 8].min()) / 1e3:.1f} us")
+
+# per-SM systematic imbalance? pass-1 duration of the CTA on each SM in both kernels
+sm_u = raw[:, 12].astype(int)
+sm_f = rf[:, 12].astype(int)
+du = {s: (raw[i, 1] - raw[i, 0]) / 1e3 for i, s in enumerate(sm_u)}
+df = {s: (rf[i, 1] - rf[i, 0]) / 1e3 for i, s in enumerate(sm_f)}
+common = sorted(set(du) & set(df))
+a = np.array([du[s] for s in common]); b = np.array([df[s] for s in common])
+print(f"pass-1 duration per SM: update {a.mean():.1f}+-{a.std():.2f} us, form {b.mean():.1f}+-{b.std():.2f} us, "
+      f"corr over {len(common)} SMs = {np.corrcoef(a, b)[0, 1]:.2f}")
+slow = sorted(common, key=lambda s: -du[s])[:8]
+print("slowest SMs (update pass 1):", slow, "form ranks:", [sorted(common, key=lambda s: -df[s]).index(s) for s in slow])
