@@ -73,6 +73,17 @@ def test_null_handle_calls_fail_cleanly(L):
     L.ig_destroy(None)
 
 
+def test_batch_calls_validate_arguments_without_a_device(L):
+    import ctypes as C
+
+    one_null = (C.c_void_p * 1)(None)
+    for fn in (L.ig_form_guess_batch, L.ig_update_batch, L.ig_form_guess_batch_host, L.ig_update_batch_host):
+        assert fn(0, None, None, None) == 0  # an empty batch is a no-op
+        assert fn(-1, None, None, None) == _lib.IG_E_ARG
+        assert fn(1, None, None, None) == _lib.IG_E_ARG
+        assert fn(1, one_null, one_null, one_null) == _lib.IG_E_ARG  # NULL handle
+
+
 def test_storage_bytes(L):
     assert L.ig_storage_bytes(1000, 1, 8) == 2 * 8 * 1024 * 8  # 2M slabs, ld rounded to 32
     assert L.ig_storage_bytes(1000, 2, 8) == 8 * 1024 * 8
