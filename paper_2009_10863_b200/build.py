@@ -41,6 +41,12 @@ def _stale(target: str, deps) -> bool:
 def build(verbose: bool = False, force: bool = False) -> str:
     os.makedirs(BUILD, exist_ok=True)
     nvcc = _nvcc()
+    # objects built with other flags (e.g. an IG_TRACE=1 debug build) are never reused
+    stamp = os.path.join(BUILD, "flags.txt")
+    want = " ".join(ARCH + FLAGS)
+    have = open(stamp).read() if os.path.exists(stamp) else None
+    if have != want:
+        force = True
     objs, jobs = [], []
     for src in SOURCES:
         s = os.path.join(CSRC, src)
@@ -71,6 +77,8 @@ def build(verbose: bool = False, force: bool = False) -> str:
             raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")
         if verbose:
             print("linked", os.path.relpath(LIB, ROOT))
+    with open(stamp, "w") as f:
+        f.write(want)
     return LIB
 
 
