@@ -172,6 +172,17 @@ void ig_comm_destroy(ig_comm_t c);
  * N is then the LOCAL slice length; ranks may have different N. */
 int ig_attach_comm(ig_t h, ig_comm_t c);
 
+/* In-process communicator: ranks that are threads of ONE process (e.g. several ranks sharing one
+ * GPU, where NCCL refuses duplicate devices).  Same all-gather semantics and layout as the NCCL
+ * communicator -- each exchange records an event on the calling handle's stream, meets the other
+ * ranks at a host barrier, and copies every rank's partial sums (device to device, after that
+ * rank's event) into the handle's gather buffer -- so the multi-rank schedule runs unchanged.
+ * Every rank must call from its own host thread, the same sequence of calls as the others.
+ * ig_local_group_create returns NULL on bad arguments; destroy the group after its comms. */
+void *ig_local_group_create(int nranks);
+void ig_local_group_destroy(void *group);
+int ig_comm_create_local(void *group, int rank, ig_comm_t *out);
+
 /* In-kernel exchange over NVLink peer memory (fused compute + collective):
  * each projection handle owns a small exchange window (ig_xwin_bytes(), < 40 KB); after every
  * reduction pass the persistent kernel's CTA 0 stores the rank-local partial sums into EVERY

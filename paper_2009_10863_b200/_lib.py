@@ -50,6 +50,9 @@ _SIGS = {
     "ig_next_slot": (_P, [_P]),
     "ig_comm_unique_id": (C.c_int, [_P]),
     "ig_comm_create": (C.c_int, [C.c_int, C.c_int, _P, C.POINTER(_P)]),
+    "ig_local_group_create": (_P, [C.c_int]),
+    "ig_local_group_destroy": (None, [_P]),
+    "ig_comm_create_local": (C.c_int, [_P, C.c_int, C.POINTER(_P)]),
     "ig_comm_destroy": (None, [_P]),
     "ig_attach_comm": (C.c_int, [_P, _P]),
     "ig_history_dim": (C.c_int, [_P, C.POINTER(C.c_int)]),

@@ -9,6 +9,7 @@
 #include <dlfcn.h>
 
 #include <atomic>
+#include <condition_variable>
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
@@ -115,9 +116,40 @@ NcclApi &nccl() {
 }
 }  // namespace
 
+// In-process rank group (ig_local_group_create): a host barrier plus the per-rank "partials
+// ready" events and source pointers of the exchange in progress.
+struct LocalGroup {
+    int n = 0;
+    std::mutex mu;
+    std::condition_variable cv;
+    int arrived = 0;
+    unsigned long long gen = 0;
+    std::vector<cudaEvent_t> ready;
+    std::vector<const double *> src;
+    explicit LocalGroup(int n_) : n(n_), ready(n_, nullptr), src(n_, nullptr) {
+        for (auto &e : ready) cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+    }
+    ~LocalGroup() {
+        for (auto e : ready)
+            if (e) cudaEventDestroy(e);
+    }
+    void barrier() {
+        std::unique_lock<std::mutex> lk(mu);
+        const unsigned long long g = gen;
+        if (++arrived == n) {
+            arrived = 0;
+            ++gen;
+            cv.notify_all();
+        } else {
+            cv.wait(lk, [&] { return gen != g; });
+        }
+    }
+};
+
 struct ig_comm_ctx {
     ncclComm_t comm = nullptr;
     int nranks = 1, rank = 0;
+    LocalGroup *local = nullptr;  // in-process group instead of NCCL
 };
 
 // ----------------------------------------------------------------------------- handle
@@ -258,6 +290,19 @@ bool use_fused(ig_t h) { return h->fused && (h->G == 1 || h->xc.G > 1); }
 
 int exchange(ig_t h, int stage) {
     if (h->G <= 1) return IG_OK;
+    if (LocalGroup *g = h->comm->local) {  // all-gather among the threads of this process
+        const int r = h->comm->rank;
+        CUDA_OK(cudaEventRecord(g->ready[r], h->stream));
+        g->src[r] = h->part + stage * PS;
+        g->barrier();  // every rank's partials are enqueued, pointers published
+        for (int q = 0; q < g->n; ++q) {
+            CUDA_OK(cudaStreamWaitEvent(h->stream, g->ready[q], 0));
+            CUDA_OK(cudaMemcpyAsync(h->gath + ((size_t)stage * h->G + q) * PS, g->src[q], sizeof(double) * PS,
+                                    cudaMemcpyDeviceToDevice, h->stream));
+        }
+        g->barrier();  // every rank has enqueued its waits: the events / pointers may be reused
+        return IG_OK;
+    }
     NcclApi &api = nccl();
     ncclResult_t r = api.allGather(h->part + stage * PS, h->gath + (size_t)stage * h->G * PS, PS, ncclFloat64,
                                    h->comm->comm, h->stream);
@@ -872,6 +917,24 @@ void ig_comm_destroy(ig_comm_t c) {
     if (!c) return;
     if (c->comm && nccl().ok) nccl().commDestroy(c->comm);
     delete c;
+}
+
+void *ig_local_group_create(int nranks) {
+    if (nranks < 1) return set_err(IG_E_ARG, "nranks must be >= 1"), nullptr;
+    return new LocalGroup(nranks);
+}
+
+void ig_local_group_destroy(void *group) { delete static_cast<LocalGroup *>(group); }
+
+int ig_comm_create_local(void *group, int rank, ig_comm_t *out) {
+    LocalGroup *g = static_cast<LocalGroup *>(group);
+    if (!g || !out || rank < 0 || rank >= g->n) return set_err(IG_E_ARG, "bad local comm arguments");
+    auto *c = new ig_comm_ctx;
+    c->nranks = g->n;
+    c->rank = rank;
+    c->local = g;
+    *out = c;
+    return IG_OK;
 }
 
 int ig_attach_comm(ig_t h, ig_comm_t c) {

@@ -240,6 +240,24 @@ def ig_comm_destroy(c) -> None:
     lib().ig_comm_destroy(c)
 
 
+def ig_local_group_create(nranks: int):
+    """In-process rank group (include/ig.h): ranks are threads of this process."""
+    g = lib().ig_local_group_create(int(nranks))
+    if not g:
+        raise IGError(IG_E_ARG, "ig_local_group_create")
+    return g
+
+
+def ig_local_group_destroy(g) -> None:
+    lib().ig_local_group_destroy(g)
+
+
+def ig_comm_create_local(group, rank: int):
+    out = C.c_void_p()
+    _check(lib().ig_comm_create_local(group, int(rank), C.byref(out)), "ig_comm_create_local")
+    return out.value
+
+
 def ig_attach_comm(h, c) -> None:
     _check(lib().ig_attach_comm(h, c), "ig_attach_comm")
 
