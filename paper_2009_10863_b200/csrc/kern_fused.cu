@@ -93,8 +93,12 @@ __global__ void __launch_bounds__(THREADS, 1) k_form_fused(ProjArgs a) {
         for (int k = 0; k < MC; ++k)
             if (k < d) v[k] = fma(a.Bt[k * a.ld + i], bv, v[k]);
     }
-    XTrip<MC, U, V> pre;  // first trip of pass 2, in flight across the barrier
-    xtrip_load(pre, a, i_first, stride, nv, d, ps);
+    // the first FP trips of pass 2 are in flight across the barrier (the bubble is ~2-4 us: one
+    // trip of 1 CTA/SM covers ~1.5 us of the SM's bandwidth share)
+    constexpr int FP = (MC <= 8) ? 2 : 1;
+    XTrip<MC, U, V> pre[FP];
+#pragma unroll
+    for (int f = 0; f < FP; ++f) xtrip_load(pre[f], a, i_first + f * U * stride, stride, nv, d, ps);
     block_partials_store<MC + 1>(v, d, false, a.blk, sh);
     TRACE_F(1);
     grid_barrier(&c->bar, 1, &c->err, a.watchdog_ns);
@@ -106,8 +110,9 @@ __global__ void __launch_bounds__(THREADS, 1) k_form_fused(ProjArgs a) {
 #pragma unroll
     for (int k = 0; k < MC; ++k) al[k] = (k < d) ? s_red[k] : 0.0;
     // ---- pass 2: x0 = X~ alpha (b fully consumed before the barrier: x0 may alias b)
-    xtrip_store(pre, a, i_first, stride, nv, al);
-    for (int64_t i0 = i_first + U * stride; i0 < nv; i0 += U * stride) {
+#pragma unroll
+    for (int f = 0; f < FP; ++f) xtrip_store(pre[f], a, i_first + f * U * stride, stride, nv, al);
+    for (int64_t i0 = i_first + FP * U * stride; i0 < nv; i0 += U * stride) {
         XTrip<MC, U, V> r;
         xtrip_load(r, a, i0, stride, nv, d, ps);
         xtrip_store(r, a, i0, stride, nv, al);
