@@ -93,8 +93,11 @@ int ig_set_admit_tol(ig_t h, double eps_rel);
  * exchange, ig_attach_peers) each ig_form_guess / ig_update is ONE persistent kernel whose passes
  * are separated by software grid barriers.  Its grid (SMs x occupancy, or ig_set_grid_limit) must
  * be resident at once: by default it is launched as an ordinary kernel (faster, PDL-chained),
- * which assumes no kernel on another stream holds SMs until this one finishes; env
- * IG_LAUNCH=coop,pdl makes the driver guarantee co-residency (cooperative launch).  A barrier
+ * which assumes no kernel on another stream holds SMs until this one finishes.  The library
+ * orders its own persistent launches across streams of one device (a launch from a different
+ * stream than the previous one waits for that stream's work; handles with a grid limit are
+ * exempt); env IG_LAUNCH=coop,pdl makes the driver guarantee co-residency against foreign
+ * kernels too (cooperative launch).  A barrier
  * that cannot complete gives up after the watchdog time (ig_set_watchdog) and reports
  * IG_E_STATE.  fused = 0, or a handle with an NCCL communicator (ig_attach_comm): one kernel per
  * pass with the NCCL exchange of partial sums between them.  Same arithmetic. */

@@ -288,6 +288,41 @@ ProjArgs proj_args(ig_t h) {
 // communicator without peer windows uses one kernel per pass with NCCL between them.
 bool use_fused(ig_t h) { return h->fused && (h->G == 1 || h->xc.G > 1); }
 
+// Full-grid persistent kernels of DIFFERENT streams on one device must not overlap: each needs its
+// whole grid resident at once (non-cooperative launch, see ig_set_schedule), and two grids whose
+// CTAs interleave could each wait at a barrier for CTAs the other one holds.  Handles sharing a
+// stream are ordered by the stream (the common case: nothing to do); a persistent launch from a
+// different stream than the previous one on this device first waits for everything enqueued on
+// that stream (one event).  Handles with a grid limit (ig_set_grid_limit: ranks sharing a GPU)
+// are exempt -- their grids are sized to be co-resident.  The lock spans the launch, so two host
+// threads cannot slip their kernels in between.
+struct PersistOrder {
+    std::mutex mu;
+    cudaStream_t last = nullptr;
+    bool any = false;
+    cudaEvent_t ev = nullptr;
+};
+PersistOrder &persist_order(int dev) {
+    static PersistOrder po[64];
+    return po[dev & 63];
+}
+template <class F> int persistent_launch(ig_t h, F &&launch) {
+    if (h->max_grid > 0) return launch();
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(h->stream, &cap) != cudaSuccess) cudaGetLastError();
+    if (cap != cudaStreamCaptureStatusNone) return launch();  // graph capture: replays order themselves
+    PersistOrder &p = persist_order(h->dev);
+    std::lock_guard<std::mutex> lk(p.mu);
+    if (p.any && p.last != h->stream) {
+        if (!p.ev) CUDA_OK(cudaEventCreateWithFlags(&p.ev, cudaEventDisableTiming));
+        if (cudaEventRecord(p.ev, p.last) == cudaSuccess) CUDA_OK(cudaStreamWaitEvent(h->stream, p.ev, 0));
+        else cudaGetLastError();  // that stream no longer exists: its work was submitted before ours
+    }
+    p.last = h->stream;
+    p.any = true;
+    return launch();
+}
+
 int exchange(ig_t h, int stage) {
     if (h->G <= 1) return IG_OK;
     if (LocalGroup *g = h->comm->local) {  // all-gather among the threads of this process
@@ -562,8 +597,12 @@ int ig_form_guess(ig_t h, const double *b, double *x0) {
         a.x0 = x0;
         const int vec = (al16(b) && al16(x0)) ? 2 : 1;
         if (use_fused(h)) {
-            Prof p(h, IG_K_FORM_FUSED);
-            CUDA_OK(launch_form_fused(a, vec, h->nsm, h->stream));
+            int rc = persistent_launch(h, [&]() -> int {
+                Prof p(h, IG_K_FORM_FUSED);
+                CUDA_OK(launch_form_fused(a, vec, h->nsm, h->stream));
+                return IG_OK;
+            });
+            if (rc) return rc;
             count(h, 1);
             return IG_OK;
         }
@@ -603,8 +642,12 @@ int ig_update(ig_t h, const double *x, const double *Ax) {
         h->known_d = -1;  // d is decided on the device
         const int vec = (al16(x) && al16(Ax)) ? 2 : 1;
         if (use_fused(h)) {
-            Prof p(h, IG_K_UPDATE_FUSED);
-            CUDA_OK(launch_update_fused(a, vec, h->nsm, h->stream));
+            int rc = persistent_launch(h, [&]() -> int {
+                Prof p(h, IG_K_UPDATE_FUSED);
+                CUDA_OK(launch_update_fused(a, vec, h->nsm, h->stream));
+                return IG_OK;
+            });
+            if (rc) return rc;
             count(h, 1);
             return IG_OK;
         }
