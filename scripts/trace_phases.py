@@ -6,18 +6,20 @@ import numpy as np, torch
 from paper_2009_10863_b200 import InitialGuess
 from paper_2009_10863_b200._lib import lib
 from workloads.gen import manufactured_step_slab
-n, M = 128, 8
+n = int(os.environ.get("TRACE_N", "128"))  # grid points per direction (n^3 DOFs); default C2
+M = int(os.environ.get("TRACE_M", "8"))
 N = n ** 3
-pool = [manufactured_step_slab(n, n, 0, 1, k, device="cuda") for k in range(14)]
+S = M + 6
+pool = [manufactured_step_slab(n, n, 0, 1, k, device="cuda") for k in range(S)]
 ig = InitialGuess(N, "proj_qr", M)
-he = InitialGuess(N, "extrap_ls", M, 3)
+he = InitialGuess(N, "extrap_ls", M, min(3, M - 1))
 x0 = torch.zeros(N, dtype=torch.float64, device="cuda")
 x0e = torch.zeros(N, dtype=torch.float64, device="cuda")
-for k in range(14):  # the bench step: QR form, QR update (traced), EXTRAP form, EXTRAP push
+for k in range(S):  # the bench step: QR form, QR update (traced), EXTRAP form, EXTRAP push
     b, x, Ax = pool[k]
     ig.form_guess(b, x0)
     ig.update(x, Ax)
-    if k < 13:
+    if k < S - 1:
         he.form_guess(None, x0e)
         he.update(x)
 torch.cuda.synchronize()
