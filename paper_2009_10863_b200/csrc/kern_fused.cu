@@ -273,37 +273,46 @@ __global__ void __launch_bounds__(THREADS, 1) k_update_fused(ProjArgs a) {
         const int64_t chunk = (int64_t)U3 * stride;
         const int64_t trips = (nv + chunk - 1) / chunk;
         const int64_t Ts = trips < 4 ? trips : trips - (trips + 7) / 8;
+        // R after this update and the next downdate's Givens plan need only c1, c2, ||b~|| and the
+        // admission.  One warp (warp 0 of CTA 0, the "planner") computes them here instead of in
+        // the serial epilogue: it stores its prefetched first trip, runs the plan (serial, cold in
+        // the instruction cache: ~6 us at M = 8, ~35 us at M = 30), and leaves its other static
+        // trips ("holes") to the dynamic claims, so the plan overlaps the whole pass.
+        const bool planner = blockIdx.x == 0 && threadIdx.x < 32 && (pend || newcol);  // warp-uniform
+        const int64_t nh = (pend || newcol) && Ts > 1 ? Ts - 1 : 0;  // the planner's trips 1..Ts-1
         if (Ts > 0) u3trip_store(pre3, a, i_first, stride, nv, deff, pend, adm, inv, c1, c2, gc, gs, pol.stream);
-        for (int64_t t = 1; t < Ts; ++t) {
-            const int64_t i0 = i_first + t * chunk;
-            U3Trip<MC, U3, V> r;
-            u3trip_load(r, a, i0, stride, nv, deff, pend, adm, pol.stream);
-            u3trip_store(r, a, i0, stride, nv, deff, pend, adm, inv, c1, c2, gc, gs, pol.stream);
-        }
-        // R after this update and the next downdate's Givens plan need only c1, c2, ||b~|| and the
-        // admission: one warp of CTA 0 computes them here, while the other warps work through the
-        // dynamically balanced tail below (~1/8 of the pass), instead of in the serial epilogue.
-        // R after this update and the next downdate's Givens plan need only c1, c2, ||b~|| and the
-        // admission: one warp of CTA 0 computes them here, while the other warps work through the
-        // dynamically balanced tail below (~1/8 of the pass), instead of in the serial epilogue
-        // (measured: 5-6 us saved per call at C2).
-        if (blockIdx.x == 0 && threadIdx.x < 32 && (pend || newcol)) {
+        if (planner) {
             TRACE(10);
             r_update_plan(c, M, deff, pend, newcol, plan, s_r1, s_r2, s_nb, s_R, s_W);
             TRACE(11);
+        } else {
+            for (int64_t t = 1; t < Ts; ++t) {
+                const int64_t i0 = i_first + t * chunk;
+                U3Trip<MC, U3, V> r;
+                u3trip_load(r, a, i0, stride, nv, deff, pend, adm, pol.stream);
+                u3trip_store(r, a, i0, stride, nv, deff, pend, adm, inv, c1, c2, gc, gs, pol.stream);
+            }
         }
+        // dynamic claims: q < nq -> the tail rows [S, nv) in 32*U3-row chunks; nq <= q < nq + nh ->
+        // the planner's static trip t = q - nq + 1 (rows t*chunk + lane + u*stride)
         const int64_t S = Ts * chunk, WCH = 32 * U3;
         const int64_t nq = nv > S ? (nv - S + WCH - 1) / WCH : 0;
-        if (nq > 0) {
+        if (nq + nh > 0) {
             const int lane = threadIdx.x & 31;
             unsigned q = (lane == 0) ? atomicAdd(&c->dyn3, 1u) : 0u;
             q = __shfl_sync(0xffffffffu, q, 0);
-            while ((int64_t)q < nq) {
+            while ((int64_t)q < nq + nh) {
                 unsigned qn = (lane == 0) ? atomicAdd(&c->dyn3, 1u) : 0u;  // claim the next one early
-                const int64_t i0 = S + (int64_t)q * WCH + lane;
                 U3Trip<MC, U3, V> r;
-                u3trip_load(r, a, i0, 32, nv, deff, pend, adm, pol.stream);
-                u3trip_store(r, a, i0, 32, nv, deff, pend, adm, inv, c1, c2, gc, gs, pol.stream);
+                if ((int64_t)q < nq) {
+                    const int64_t i0 = S + (int64_t)q * WCH + lane;
+                    u3trip_load(r, a, i0, 32, nv, deff, pend, adm, pol.stream);
+                    u3trip_store(r, a, i0, 32, nv, deff, pend, adm, inv, c1, c2, gc, gs, pol.stream);
+                } else {
+                    const int64_t i0 = ((int64_t)q - nq + 1) * chunk + lane;
+                    u3trip_load(r, a, i0, stride, nv, deff, pend, adm, pol.stream);
+                    u3trip_store(r, a, i0, stride, nv, deff, pend, adm, inv, c1, c2, gc, gs, pol.stream);
+                }
                 q = __shfl_sync(0xffffffffu, qn, 0);
             }
         }
