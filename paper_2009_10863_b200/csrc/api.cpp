@@ -569,7 +569,7 @@ int ig_load_state(ig_t h, const void *host_buf, size_t bytes) {
         Ctrl c;
         memcpy(&c, p, sizeof c);
         for (unsigned &t : c.ticket) t = 0;  // transient launch state is never part of a checkpoint
-        c.bar = c.bar_exit = c.dyn3 = 0;
+        c.bar[0] = c.bar[1] = c.dyn3[0] = c.dyn3[1] = 0;
         c.err = 0;
         CUDA_OK(cudaMemcpyAsync(h->ctrl, &c, sizeof c, cudaMemcpyHostToDevice, h->stream));
         CUDA_OK(cudaStreamSynchronize(h->stream));  // c is a stack object

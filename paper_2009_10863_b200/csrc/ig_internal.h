@@ -46,8 +46,13 @@ struct Ctrl {
     int last_rot;   // the last update applied a downdate (bytes accounting)
     int err;        // failure detection: 0 ok, 1 grid-barrier / 2 peer-exchange timeout, 3 non-finite sums
     unsigned ticket[NSTAGE];
-    unsigned bar, bar_exit;        // grid barrier / exit counters of the fused kernels
-    unsigned dyn3, dyn_pad_;       // work-claim counter of the dynamically balanced pass-3 tail
+    // Persistent fused kernels: launch epoch e (bumped once per launch that uses a grid barrier);
+    // launch e uses the barrier and work-claim counters of parity e & 1 and zeroes those of parity
+    // (e + 1) & 1 for the next launch, so no CTA has to wait for the others at exit.
+    unsigned epoch;
+    unsigned bar[2];               // grid-barrier arrival counters
+    unsigned dyn3[2];              // work-claim counters of the dynamically balanced pass-3 tail
+    unsigned epoch_pad_;
     unsigned long long xepoch[NSTAGE];  // completed peer exchanges per stage (all ranks agree)
     double rho, nAx, nb;
     double gc[MAXM], gs[MAXM];      // Givens (c_i, s_i) of the pending downdate

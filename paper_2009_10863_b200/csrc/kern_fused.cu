@@ -60,6 +60,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_form_fused(ProjArgs a) {
     Ctrl *c = a.ctrl;
     const int d = c->d;
     if (d == 0) return;  // uniform: x0 stays the caller's fallback
+    const unsigned e = launch_epoch(c);
     const unsigned long long ep = c->xepoch[ST_FORM] + 1;
     // All form traffic is single-use within the call (the caller's solve runs next): evict_first,
     // so the guess does not push the solver's working set out of L2.
@@ -101,7 +102,8 @@ __global__ void __launch_bounds__(THREADS, 1) k_form_fused(ProjArgs a) {
     for (int f = 0; f < FP; ++f) xtrip_load(pre[f], a, i_first + f * U * stride, stride, nv, d, ps);
     block_partials_store<MC + 1>(v, d, false, a.blk, sh);
     TRACE_F(1);
-    grid_barrier(&c->bar, 1, &c->err, a.watchdog_ns);
+    grid_barrier(&c->bar[e & 1], 1, &c->err, a.watchdog_ns);
+    advance_epoch(c, e);
     TRACE_F(2);
     reduce_all_blocks<MC>(d, false, a.blk, s_red);
     TRACE_F(3);
@@ -127,8 +129,9 @@ __global__ void __launch_bounds__(THREADS, 1) k_form_fused(ProjArgs a) {
     }
     TRACE_F(4);
     pdl_trigger();
-    if (grid_exit(&c->bar, &c->bar_exit)) {
-        TRACE_F(9);
+    // epilogue: every CTA holds the same sums, so CTA 0 writes the control block without waiting
+    // for the others (the next kernel sees it after this grid completes)
+    if (blockIdx.x == 0) {
         if (threadIdx.x < d) a.part[ST_FORM * PS + threadIdx.x] = s_red[threadIdx.x];
         if (threadIdx.x < d && !isfinite(s_red[threadIdx.x])) watchdog_trip(&c->err, 3);
         if (threadIdx.x == 0 && a.xc.G > 1) c->xepoch[ST_FORM] = ep;
@@ -158,6 +161,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_update_fused(ProjArgs a) {
     }
 #endif
     Ctrl *c = a.ctrl;
+    const unsigned e = launch_epoch(c);
     const int d = c->d, M = a.M;
     const bool pend = c->pending != 0;
     const bool restart = (a.method == M_PROJ_CLASSIC) && (d >= M);  // Alg. 1 restart
@@ -203,7 +207,8 @@ __global__ void __launch_bounds__(THREADS, 1) k_update_fused(ProjArgs a) {
     if (deff > 0 && ntrip2 > 0) u2trip_load(pre2, a, i_first + (ntrip2 - 1) * UB * stride, stride, nv, deff, pol.keep);
     block_partials_store<MC + 1>(v, deff, true, a.blk, sh);
     TRACE(1);
-    grid_barrier(&c->bar, 1, &c->err, a.watchdog_ns);
+    grid_barrier(&c->bar[e & 1], 1, &c->err, a.watchdog_ns);
+    advance_epoch(c, e);
     TRACE(2);
     reduce_all_blocks<MC>(deff, true, a.blk, s_r1);
     TRACE(3);
@@ -234,7 +239,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_update_fused(ProjArgs a) {
     u3trip_load(pre3, a, i_first, stride, nv, deff, pend, true, pol.stream);
     if (deff > 0) block_partials_store<MC + 1>(v, deff, true, a.blk + BLK2, sh);
     TRACE(4);
-    grid_barrier(&c->bar, 2, &c->err, a.watchdog_ns);
+    grid_barrier(&c->bar[e & 1], 2, &c->err, a.watchdog_ns);
     TRACE(5);
     if (deff > 0) reduce_all_blocks<MC>(deff, true, a.blk + BLK2, s_r2);
     if (deff > 0 && a.xc.G > 1) peer_allreduce(a.xc, ST_U2, deff, true, s_r2, ep2, &c->err, a.watchdog_ns);
@@ -299,10 +304,10 @@ __global__ void __launch_bounds__(THREADS, 1) k_update_fused(ProjArgs a) {
         const int64_t nq = nv > S ? (nv - S + WCH - 1) / WCH : 0;
         if (nq + nh > 0) {
             const int lane = threadIdx.x & 31;
-            unsigned q = (lane == 0) ? atomicAdd(&c->dyn3, 1u) : 0u;
+            unsigned q = (lane == 0) ? atomicAdd(&c->dyn3[e & 1], 1u) : 0u;
             q = __shfl_sync(0xffffffffu, q, 0);
             while ((int64_t)q < nq + nh) {
-                unsigned qn = (lane == 0) ? atomicAdd(&c->dyn3, 1u) : 0u;  // claim the next one early
+                unsigned qn = (lane == 0) ? atomicAdd(&c->dyn3[e & 1], 1u) : 0u;  // claim the next one early
                 U3Trip<MC, U3, V> r;
                 if ((int64_t)q < nq) {
                     const int64_t i0 = S + (int64_t)q * WCH + lane;
@@ -324,8 +329,10 @@ __global__ void __launch_bounds__(THREADS, 1) k_update_fused(ProjArgs a) {
     }
     TRACE(6);
     pdl_trigger();
-    // ---- epilogue (last CTA out): control block
-    if (!grid_exit(&c->bar, &c->bar_exit)) {
+    // ---- epilogue: every CTA holds the same sums and decisions, so CTA 0 writes the control
+    // block without waiting for the others (every CTA read it before barrier 1; the next kernel
+    // sees it after this grid completes).  No exit barrier, no fence drain on the critical path.
+    if (blockIdx.x != 0) {
         TRACE(7);
         return;
     }
@@ -340,7 +347,6 @@ __global__ void __launch_bounds__(THREADS, 1) k_update_fused(ProjArgs a) {
         bool fin = isfinite(s_r1[NORM]) && (deff == 0 || isfinite(s_r2[NORM]));
         for (int k = 0; k < deff; ++k) fin = fin && isfinite(s_r1[k]) && isfinite(s_r2[k]);
         if (!fin) watchdog_trip(&c->err, 3);
-        c->dyn3 = 0;  // every other CTA has left: no claims in flight
         c->d = dnew;
         c->deff = deff;
         c->pending = plan ? 1 : 0;

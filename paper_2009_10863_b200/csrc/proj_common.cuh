@@ -196,10 +196,10 @@ __device__ __forceinline__ unsigned ld_acquire_u32(const unsigned *p) {
     return v;
 }
 
-// Software grid barrier for a co-resident (cooperatively launched) grid.  `ctr` counts arrivals
-// monotonically within one launch; barrier number `phase` (1, 2, ...) waits for phase*gridDim
-// arrivals.  The last CTA to leave the kernel resets the counters (grid_exit), so the next launch
-// (stream-ordered) starts from zero: safe under CUDA-graph replay.
+// Software grid barrier for a co-resident grid.  `ctr` (the launch epoch's parity counter,
+// zeroed by the previous launch, see Ctrl::epoch) counts arrivals monotonically within one launch;
+// barrier number `phase` (1, 2, ...) waits for phase*gridDim arrivals.  Safe under CUDA-graph
+// replay: the epoch lives in device memory.
 __device__ __forceinline__ unsigned long long globaltimer_ns() {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -230,21 +230,20 @@ __device__ __forceinline__ void grid_barrier(unsigned *ctr, unsigned phase, int 
     __syncthreads();
 }
 
-// Returns true in the last CTA to exit; that CTA owns the control-block epilogue and resets
-// the barrier counters.
-__device__ __forceinline__ bool grid_exit(unsigned *ctr, unsigned *exit_ctr) {
-    __shared__ unsigned s_t;
-    __threadfence();
-    __syncthreads();
-    if (threadIdx.x == 0) s_t = atomicAdd(exit_ctr, 1u);
-    __syncthreads();
-    if (s_t != gridDim.x - 1) return false;
-    __threadfence();
-    if (threadIdx.x == 0) {
-        *ctr = 0;
-        *exit_ctr = 0;
+// Launch epoch of a persistent fused kernel (call after pdl_wait, before the first barrier, in
+// every CTA): CTA 0 zeroes the counters of the NEXT epoch's parity (the launch that used them
+// last has completed: stream order).  Returns this launch's epoch.
+__device__ __forceinline__ unsigned launch_epoch(Ctrl *c) {
+    const unsigned e = *(volatile unsigned *)&c->epoch;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        c->bar[(e + 1) & 1] = 0;
+        c->dyn3[(e + 1) & 1] = 0;
     }
-    return true;
+    return e;
+}
+// After the first barrier every CTA has read the epoch: CTA 0 advances it for the next launch.
+__device__ __forceinline__ void advance_epoch(Ctrl *c, unsigned e) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) c->epoch = e + 1;
 }
 
 // Every CTA reduces all block partials of a stage in the same fixed order (so all CTAs hold

@@ -29,7 +29,7 @@ buf = (C.c_ulonglong * (1024 * 16))()
 assert L.ig_debug_trace_read(buf, 1024 * 16) == 0
 raw = np.array(buf[:148 * 16], dtype=np.float64).reshape(148, 16)
 t = raw[:, [8, 0, 1, 2, 3, 4, 5, 6, 7]]
-last = int(np.argmax(raw[:, 7]))  # the CTA that ran the epilogue
+last = 0  # CTA 0 writes the control block (no exit barrier)
 t0 = t[:, 0].min()
 t = (t - t0) / 1e3  # us
 names = ["CTA begin", "pdl_wait out", "pass1 done", "barrier1 out", "reduce1 done", "pass2 done", "barrier2 out", "pass3 done",
@@ -37,7 +37,7 @@ names = ["CTA begin", "pdl_wait out", "pass1 done", "barrier1 out", "reduce1 don
 for j, nm in enumerate(names):
     print(f"{nm:14s} min {t[:, j].min():8.1f} med {np.median(t[:, j]):8.1f} max {t[:, j].max():8.1f} us")
 e = (raw[last, [6, 9, 7]] - t0) / 1e3
-print(f"epilogue CTA {last}: pass3 done {e[0]:.1f}, after grid_exit {e[1]:.1f}, done {e[2]:.1f} us")
+print(f"CTA 0 (planner + control block): pass3 done {e[0]:.1f}, epilogue start {e[1]:.1f}, done {e[2]:.1f} us")
 pl = (raw[0, [10, 11]] - t0) / 1e3
 print(f"R update + Givens plan (CTA 0 warp 0, during pass 3): {pl[0]:.1f} -> {pl[1]:.1f} us ({pl[1] - pl[0]:.1f} us)")
 
@@ -49,8 +49,6 @@ tf = (rf[:, [8, 0, 1, 2, 3, 4, 7]] - rf[:, 8].min()) / 1e3
 print("k_form_fused:")
 for j, nm in enumerate(["CTA begin", "pdl_wait out", "pass1 done", "barrier out", "reduce done", "pass2 done", "exit"]):
     print(f"  {nm:14s} min {tf[:, j].min():8.1f} med {np.median(tf[:, j]):8.1f} max {tf[:, j].max():8.1f} us")
-lf = int(np.argmax(rf[:, 7]))
-print(f"  last CTA {lf}: after grid_exit {(rf[lf, 9] - rf[:, 8].min()) / 1e3:.1f} us")
 
 # per-SM systematic imbalance? pass-1 duration of the CTA on each SM in both kernels
 sm_u = raw[:, 12].astype(int)
