@@ -235,8 +235,11 @@ __global__ void __launch_bounds__(THREADS, 1) k_update_fused(ProjArgs a) {
             u2trip_compute(r, c1, v);
         }
     }
-    U3Trip<MC, U3, V> pre3;  // first trip of pass 3, in flight across barrier 2
-    u3trip_load(pre3, a, i_first, stride, nv, deff, pend, true, pol.stream);
+    // first trip of pass 3, in flight across barrier 2 -- except in warp 0 of CTA 0, which may
+    // become the Givens planner (see pass 3) and then hands all its trips to the dynamic claims
+    const bool w0 = blockIdx.x == 0 && threadIdx.x < 32;
+    U3Trip<MC, U3, V> pre3;
+    if (!w0) u3trip_load(pre3, a, i_first, stride, nv, deff, pend, true, pol.stream);
     if (deff > 0) block_partials_store<MC + 1>(v, deff, true, a.blk + BLK2, sh);
     TRACE(4);
     grid_barrier(&c->bar[e & 1], 2, &c->err, a.watchdog_ns);
@@ -280,17 +283,20 @@ __global__ void __launch_bounds__(THREADS, 1) k_update_fused(ProjArgs a) {
         const int64_t Ts = trips < 4 ? trips : trips - (trips + 7) / 8;
         // R after this update and the next downdate's Givens plan need only c1, c2, ||b~|| and the
         // admission.  One warp (warp 0 of CTA 0, the "planner") computes them here instead of in
-        // the serial epilogue: it stores its prefetched first trip, runs the plan (serial, cold in
-        // the instruction cache: ~6 us at M = 8, ~35 us at M = 30), and leaves its other static
-        // trips ("holes") to the dynamic claims, so the plan overlaps the whole pass.
-        const bool planner = blockIdx.x == 0 && threadIdx.x < 32 && (pend || newcol);  // warp-uniform
-        const int64_t nh = (pend || newcol) && Ts > 1 ? Ts - 1 : 0;  // the planner's trips 1..Ts-1
-        if (Ts > 0) u3trip_store(pre3, a, i_first, stride, nv, deff, pend, adm, inv, c1, c2, gc, gs, pol.stream);
+        // the serial epilogue: it runs the plan (serial, cold in the instruction cache: ~5 us at
+        // M = 8, ~35 us at M = 30) right after barrier 2 and leaves all its static trips
+        // ("holes") to the dynamic claims, so the plan overlaps the whole pass.
+        const bool planner = w0 && (pend || newcol);  // warp-uniform
+        const int64_t nh = (pend || newcol) ? Ts : 0;  // the planner's trips 0..Ts-1
         if (planner) {
             TRACE(10);
             r_update_plan(c, M, deff, pend, newcol, plan, s_r1, s_r2, s_nb, s_R, s_W);
             TRACE(11);
         } else {
+            if (Ts > 0) {
+                if (w0) u3trip_load(pre3, a, i_first, stride, nv, deff, pend, adm, pol.stream);
+                u3trip_store(pre3, a, i_first, stride, nv, deff, pend, adm, inv, c1, c2, gc, gs, pol.stream);
+            }
             for (int64_t t = 1; t < Ts; ++t) {
                 const int64_t i0 = i_first + t * chunk;
                 U3Trip<MC, U3, V> r;
@@ -299,7 +305,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_update_fused(ProjArgs a) {
             }
         }
         // dynamic claims: q < nq -> the tail rows [S, nv) in 32*U3-row chunks; nq <= q < nq + nh ->
-        // the planner's static trip t = q - nq + 1 (rows t*chunk + lane + u*stride)
+        // the planner's static trip t = q - nq (rows t*chunk + lane + u*stride)
         const int64_t S = Ts * chunk, WCH = 32 * U3;
         const int64_t nq = nv > S ? (nv - S + WCH - 1) / WCH : 0;
         if (nq + nh > 0) {
@@ -314,7 +320,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_update_fused(ProjArgs a) {
                     u3trip_load(r, a, i0, 32, nv, deff, pend, adm, pol.stream);
                     u3trip_store(r, a, i0, 32, nv, deff, pend, adm, inv, c1, c2, gc, gs, pol.stream);
                 } else {
-                    const int64_t i0 = ((int64_t)q - nq + 1) * chunk + lane;
+                    const int64_t i0 = ((int64_t)q - nq) * chunk + lane;
                     u3trip_load(r, a, i0, stride, nv, deff, pend, adm, pol.stream);
                     u3trip_store(r, a, i0, stride, nv, deff, pend, adm, inv, c1, c2, gc, gs, pol.stream);
                 }
