@@ -9,12 +9,16 @@ Workload (BASELINE.json configs[1], "C2"): 3D 128^3 7-point Helmholtz manufactur
 time steps.  One STEP = the whole hot path once: QR form + QR update + EXTRAP form + EXTRAP
 update (push by copy) on that step's fresh (b_n, x_n, A x_n), all resident in HBM.
 With N > 1 every rank holds a contiguous z-slab of 128^3 DOFs of a 128x128x(128N) global
-problem (weak scaling); the projection's global sums go over NCCL, extrapolation never
-communicates.
+problem (weak scaling); the projection's global sums go through the in-kernel NVLink peer
+exchange (--exchange peer, default; NCCL all-gather between kernels with --exchange nccl or when
+the GPUs lack P2P), extrapolation never communicates.  --config c3|c4 selects configs[2]/[3].
 
 value = effective HBM GB/s of the whole job = (algorithmic bytes of all ranks) / (max-over-ranks
-device time), algorithmic bytes per step and rank = [(8M+4) + (M+1) + 2] * 8 * N (DESIGN.md
-"Bytes").  ms_per_step is reported beside it.
+device time), algorithmic bytes per step and rank = [(8M+4) + (nnz(beta)+1) + 2] * 8 * N
+(DESIGN.md section 7).  ms_per_step is reported beside it.  Also on the JSON line: roofline (the
+dominant kernel against the measured copy peak, plus read-only and nominal ceilings), kernels
+(per-kernel event timing from a second pass), step_stats, fill_phase, clocks, e2e (host-buffer
+batch calls, PCIe transfers inside the timed region), cpu_baseline (the CPU oracle).
 """
 
 from __future__ import annotations
