@@ -45,6 +45,7 @@ struct Ctrl {
     int admitted;   // last update admitted its pair
     int last_rot;   // the last update applied a downdate (bytes accounting)
     int err;        // failure detection: 0 ok, 1 grid-barrier / 2 peer-exchange timeout, 3 non-finite sums
+    int d_in;       // d at the start of the current update (split schedule: u1 overwrites d)
     unsigned ticket[NSTAGE];
     // Persistent fused kernels: launch epoch e (bumped once per launch that uses a grid barrier);
     // launch e uses the barrier and work-claim counters of parity e & 1 and zeroes those of parity
@@ -52,7 +53,6 @@ struct Ctrl {
     unsigned epoch;
     unsigned bar[2];               // grid-barrier arrival counters
     unsigned dyn3[2];              // work-claim counters of the dynamically balanced pass-3 tail
-    unsigned epoch_pad_;
     unsigned long long xepoch[NSTAGE];  // completed peer exchanges per stage (all ranks agree)
     double rho, nAx, nb;
     double gc[MAXM], gs[MAXM];      // Givens (c_i, s_i) of the pending downdate

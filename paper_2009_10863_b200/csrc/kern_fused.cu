@@ -270,7 +270,9 @@ __global__ void __launch_bounds__(THREADS, 1) k_update_fused(ProjArgs a) {
 #pragma unroll
         for (int k = 0; k < MC; ++k) c2r[k] = s_c2[k];
     }
-    const int dnew = deff + (adm ? 1 : 0);
+    // a zero A x is skipped (AMB-6); for CLASSIC at d >= M that includes the restart:
+    // the full history is kept (Alg. 1's restart branch divides by ||b~||)
+    const int dnew = (restart && !adm) ? d : deff + (adm ? 1 : 0);
     const bool newcol = a.method == M_PROJ_QR && adm;  // R_{1:d,d+1} = c1 + c2, R_{d+1,d+1} = ||b~||
     const bool plan = a.method == M_PROJ_QR && dnew == M;  // the next update downdates
     // ---- pass 3: [Givens rotation of X~] + store the admitted pair

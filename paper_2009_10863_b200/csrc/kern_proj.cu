@@ -149,6 +149,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_u1(ProjArgs a) {
             c->deff = deff;
             c->rotX = pend ? 1 : 0;
             c->pending = 0;
+            c->d_in = d;
             c->d = deff;  // downdate: d <- M-1; classic restart: d <- 0
             c->ticket[ST_U1] = 0;
         }
@@ -267,7 +268,10 @@ __global__ void __launch_bounds__(THREADS, 1) k_u3(ProjArgs a) {
     __syncthreads();
     if (s_ticket != gridDim.x - 1) return;
     __threadfence();
-    const int dnew = deff + (adm ? 1 : 0);
+    // a zero A x is skipped (AMB-6); for CLASSIC at d >= M that includes the restart (see kern_fused.cu)
+    const int d_in = c->d_in;
+    const bool restart = a.method == M_PROJ_CLASSIC && d_in >= M;
+    const int dnew = (restart && !adm) ? d_in : deff + (adm ? 1 : 0);
     if (a.method == M_PROJ_QR && adm) {  // R_{1:d,d+1} = c1 + c2, R_{d+1,d+1} = ||b~||
         for (int k = threadIdx.x; k < MAXM; k += blockDim.x)
             c->R[k + deff * MAXM] = (k < deff) ? s_c1[k] + s_c2[k] : (k == deff ? s_nb : 0.0);
