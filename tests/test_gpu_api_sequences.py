@@ -46,8 +46,10 @@ def test_random_call_sequences_match_oracle(seed, n):
     hs = [InitialGuess(N, m, M, p) for m, M, p in SPECS]
     oras = [_oracle(m, N, M, p) for m, M, p in SPECS]
     fused = [True] * len(SPECS)
+    from paper_2009_10863_b200 import ig_form_guess_batch, ig_update_batch
+
     ops = ["form", "form", "update", "update", "update", "update_zero", "update_repeat", "reset", "save_load",
-           "schedule", "form_host", "update_host"]
+           "schedule", "form_host", "update_host", "update_inplace", "form_batch", "update_batch"]
     last = [None] * len(SPECS)
     checked = 0
     for step in range(70):
@@ -56,7 +58,29 @@ def test_random_call_sequences_match_oracle(seed, n):
         h, o = hs[i], oras[i]
         op = ops[int(rng.integers(len(ops)))]
         b, x, Ax = seq[int(rng.integers(len(seq)))]
-        if op in ("form", "form_host"):
+        if op == "form_batch":  # every field at once (one time step of a multi-field solver)
+            fbs = [rng.standard_normal(N) for _ in SPECS]
+            x0s = [torch.from_numpy(f).cuda() for f in fbs]
+            bs = [torch.from_numpy(b).cuda() if m.startswith("proj") else None for m, _, _ in SPECS]
+            ig_form_guess_batch(hs, bs, x0s)
+            for k, (oo, f, x0) in enumerate(zip(oras, fbs, x0s)):
+                ref = oo.form_guess(b, f)
+                nr = np.linalg.norm(ref)
+                assert np.linalg.norm(x0.cpu().numpy() - ref) <= TOL * (nr if nr > 0 else 1.0), (seed, step, op, k)
+            checked += 1
+        elif op == "update_batch":
+            ig_update_batch(hs, [torch.from_numpy(x).cuda() for _ in SPECS],
+                            [torch.from_numpy(Ax).cuda() if m.startswith("proj") else None for m, _, _ in SPECS])
+            for k, oo in enumerate(oras):
+                oo.update(x, Ax)
+                last[k] = (x, Ax)
+        elif op == "update_inplace" and method == "extrap_ls":  # the solver wrote x into the slot
+            slot = h.next_slot()
+            slot.copy_(torch.from_numpy(x).cuda())
+            h.update(slot)
+            o.update(x, Ax)
+            last[i] = (x, Ax)
+        elif op in ("form", "form_host"):
             fb = rng.standard_normal(N)
             ref = o.form_guess(b, fb)
             if op == "form":
