@@ -79,10 +79,19 @@ template <int VEC>
 __global__ void __launch_bounds__(THREADS, 1) k_copy(double *__restrict__ dst, const double *__restrict__ src, int64_t N) {
     pdl_wait();
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    if (VEC == 2) {
+    if (VEC == 2) {  // 4 strided 16-byte loads in flight per thread, then the 4 stores
+        constexpr int U = 4;
         const int64_t nv = N >> 1;
-        for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nv; i += stride)
-            reinterpret_cast<double2 *>(dst)[i] = __ldg(reinterpret_cast<const double2 *>(src) + i);
+        const double2 *s2 = reinterpret_cast<const double2 *>(src);
+        double2 *d2 = reinterpret_cast<double2 *>(dst);
+        for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i0 < nv; i0 += U * stride) {
+            double2 r[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) r[u] = (i0 + u * stride < nv) ? __ldg(s2 + i0 + u * stride) : make_double2(0.0, 0.0);
+#pragma unroll
+            for (int u = 0; u < U; ++u)
+                if (i0 + u * stride < nv) d2[i0 + u * stride] = r[u];
+        }
         if ((N & 1) && blockIdx.x == 0 && threadIdx.x == 0) dst[N - 1] = src[N - 1];
     } else {
         for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < N; i += stride) dst[i] = src[i];
