@@ -112,3 +112,54 @@ def test_paper_ordering_of_methods():
     ex, _ = _run(g, 40, lambda: ExtrapLS(g.N, 8, 3), lambda: InitialGuess(g.N, "extrap_ls", 8, 3))
     tail = slice(10, None)  # after the histories filled
     assert qr[tail].mean() < ex[tail].mean() < last[tail].mean(), (qr.mean(), ex.mean(), last.mean())
+
+
+# Second workload: one time step of an INS-like solver
+# = three velocity components solved with a Helmholtz operator of large shift (gamma/(nu dt)),
+# guessed by EXTRAP, plus a pressure Poisson solve (sigma = 0), guessed by QR -- four history
+# spaces, one batched guess call and one batched update call per step.  Downstream iterations of
+# every field on identical systems within +-1 of the oracle; the pressure projection must beat
+# LAST by a wide margin and the velocity extrapolation must not lose to LAST.
+def test_velocity_pressure_fields_batched():
+    from paper_2009_10863_b200 import InitialGuess, ig_form_guess_batch, ig_update_batch
+
+    n, steps, dt = 32, 30, 1e-3
+    gv = Grid(n, 2, sigma=1e3)  # velocity Helmholtz: shift gamma/(nu dt) dominates the Laplacian less than fully
+    gp = Grid(n, 2, sigma=0.0)  # pressure Poisson
+    grids = [gv, gv, gv, gp]
+    specs = [("extrap_ls", 4, 2), ("extrap_ls", 4, 2), ("extrap_ls", 4, 2), ("proj_qr", 8, 0)]
+    oras = [ExtrapLS(gv.N, 4, 2) for _ in range(3)] + [ProjQR(gp.N, 8)]
+    libs = [InitialGuess(g.N, m, M, p) for g, (m, M, p) in zip(grids, specs)]
+    offs = [0, 7, 13, 0]  # the velocity components see different (time-shifted) forcings
+    x_prev = [torch.zeros(g.N, dtype=torch.float64) for g in grids]
+    its = {"ora": [[] for _ in grids], "gpu": [[] for _ in grids], "last": [[] for _ in grids]}
+    for t in range(steps):
+        bs = [prescribed_rhs(g, t + o, dt) for g, o in zip(grids, offs)]
+        x0g = [xp.clone().cuda() for xp in x_prev]
+        ig_form_guess_batch(libs, [b.cuda() if m.startswith("proj") else None for b, (m, _, _) in zip(bs, specs)], x0g)
+        xs, Axs = [], []
+        for k, (g, b, o) in enumerate(zip(grids, bs, oras)):
+            x0o = torch.from_numpy(o.form_guess(b.numpy(), x_prev[k].numpy()))
+            x, it_o, _, _ = pcg(g, b, x0o)
+            _, it_g, _, _ = pcg(g, b, x0g[k].cpu())
+            _, it_l, _, _ = pcg(g, b, x_prev[k])
+            its["ora"][k].append(it_o)
+            its["gpu"][k].append(it_g)
+            its["last"][k].append(it_l)
+            Ax = helmholtz_apply(g, x)
+            o.update(x.numpy(), Ax.numpy())
+            xs.append(x)
+            Axs.append(Ax)
+            x_prev[k] = x
+        ig_update_batch(libs, [x.cuda() for x in xs], [Ax.cuda() if m.startswith("proj") else None
+                                                         for Ax, (m, _, _) in zip(Axs, specs)])
+    for h in libs:
+        h.close()
+    for k in range(len(grids)):
+        d = np.abs(np.array(its["gpu"][k]) - np.array(its["ora"][k]))
+        assert d.max() <= 1, (k, its["gpu"][k], its["ora"][k])
+    warm = slice(10, None)
+    p_qr, p_last = np.mean(its["gpu"][3][warm]), np.mean(its["last"][3][warm])
+    assert p_qr < 0.5 * p_last, (p_qr, p_last)
+    for k in range(3):
+        assert np.mean(its["gpu"][k][warm]) <= np.mean(its["last"][k][warm]), k
