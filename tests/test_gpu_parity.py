@@ -501,6 +501,10 @@ def test_admission_tolerance_parity(eps):
         ora.update(x, Ax)
         ig.update(torch.from_numpy(x).cuda(), torch.from_numpy(Ax).cuda())
         st = ig.stats()
+        # a decision with |rho/eps - 1| < 1e-9 is ill-posed (rounding may flip it);
+        # the sequence must not contain one, or the exact comparison below would mean nothing
+        assert eps == 0.0 or abs(ora.rho / eps - 1.0) > 1e-9
+        assert abs(st["rho"] - ora.rho) <= 1e-7 * max(ora.rho, 1e-300)  # same rho (cancellation-limited)
         assert (st["d"], bool(st["admitted"])) == (ora.d, ora.admitted)
         ds.append(ora.d)
     if eps >= 1e-4:
