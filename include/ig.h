@@ -20,9 +20,11 @@
  *   - Return value: IG_OK (0) or an ig_status code; ig_last_error() gives a thread-local message.
  *   - A handle is used by one host thread at a time.  Handles are independent (one per field,
  *     PAPER.md:903-907).
- *   - Multi-GPU: every rank calls the same sequence with its contiguous DOF slice; after
- *     ig_attach_comm the projection's global sums are exchanged with NCCL (all-gather of the
- *     per-rank partial sums, summed in rank order: bitwise-identical decisions on all ranks).
+ *   - Multi-GPU: every rank calls the same sequence with its contiguous DOF slice.  The
+ *     projection's global sums are exchanged either inside the persistent kernels over NVLink
+ *     peer memory (ig_attach_peers) or between kernels by an all-gather (ig_attach_comm: NCCL,
+ *     or ig_comm_create_local for ranks that are threads of one process); either way the
+ *     per-rank partial sums are summed in rank order: bitwise-identical decisions on all ranks.
  *     Extrapolation never communicates.
  */
 #ifndef IG_H
