@@ -567,11 +567,14 @@ def run_ours(args, world, rank, local):
 
 def main():
     args = parse()
-    world, rank, local = dist_setup(args)
     if args.impl == "reference":
+        # the reference arm is the CPU oracle on rank 0 only: no process group, no GPU; the other
+        # ranks of a torchrun launch exit 0 without work
+        world, rank = int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("RANK", "0"))
         run_reference(args, world, rank)
-    else:
-        run_ours(args, world, rank, local)
+        return
+    world, rank, local = dist_setup(args)
+    run_ours(args, world, rank, local)
     if world > 1:
         import torch.distributed as dist
 
