@@ -6,7 +6,7 @@ resets, checkpoint -> restore into a fresh handle, switching between the fused a
 schedule, device- and host-buffer entry points.  Every guess within 1e-11 of the oracle
 (PAPER.md:253-308 for QR / CLASSIC, Eq. EXTRAPEXPN for EXTRAP)."""
 
-import copy
+import os
 
 import numpy as np
 import pytest
@@ -32,8 +32,12 @@ def _oracle(method, N, M, p):
             "extrap_ls": lambda: ExtrapLS(N, M, p)}[method]()
 
 
+_EXTRA = int(os.environ.get("IG_SEQ_SEEDS", "0"))  # soak: IG_SEQ_SEEDS=50 adds 50 more sequences
+
+
 @pytest.mark.timeout(300)
-@pytest.mark.parametrize("seed,n", [(1, 27), (2, 27), (3, 27), (4, 27), (5, 600), (6, 600)])
+@pytest.mark.parametrize("seed,n", [(1, 27), (2, 27), (3, 27), (4, 27), (5, 600), (6, 600)]
+                         + [(100 + k, 27 if k % 3 else 600) for k in range(_EXTRA)])
 def test_random_call_sequences_match_oracle(seed, n):
     """n = 27: one grid-stride trip per thread; n = 600 (360,000 DOFs): several trips, so the
     dynamically claimed pass-3 tail and the Givens planner's handed-off trips are exercised."""
