@@ -106,3 +106,17 @@ def test_product_package_never_imports_oracle():
             if f.endswith((".py", ".cu", ".cpp", ".h")):
                 txt = open(os.path.join(dp, f)).read()
                 assert "oracle" not in re.sub(r"(#|//).*", "", txt).replace("oracle/", ""), f
+
+
+def test_missing_library_fails_loudly(monkeypatch, tmp_path):
+    """No CPU fallback anywhere in the product path: without libig.so every call raises."""
+    import pytest
+
+    monkeypatch.setattr(_lib, "LIB_PATH", str(tmp_path / "libig.so"))
+    monkeypatch.setattr(_lib, "_lib", None)
+    with pytest.raises(RuntimeError, match="no CPU fallback"):
+        _lib.lib()
+    from paper_2009_10863_b200 import ig
+
+    with pytest.raises(RuntimeError, match="no CPU fallback"):
+        ig.ig_total_launches()
