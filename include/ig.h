@@ -121,6 +121,10 @@ int ig_form_guess(ig_t h, const double *b, double *x0);
  *     apply).  If d == M the oldest pair is dropped by a Givens QR downdate; then
  *     (x, Ax) is orthogonalised by twice-iterated classical Gram-Schmidt and admitted iff
  *     ||b~|| > eps*||Ax|| (d == 0: admitted iff ||Ax|| > 0).
+ *     A zero Ax is skipped (d == 0; CLASSIC also at d >= M: no restart).  The sums (||Ax||^2,
+ *     the Gram-Schmidt coefficients) are plain fp64 without scaling: ||A x||^2 must stay finite
+ *     (entries below ~1e150 in magnitude); NaN/Inf sums leave the pair unadmitted and are
+ *     reported as IG_E_STATE by the next synchronising call.
  *   Extrapolation: x is pushed into the solution window (Ax ignored, may be NULL).  If
  *     x == ig_next_slot(h) nothing is copied; otherwise one copy. */
 int ig_update(ig_t h, const double *x, const double *Ax);
