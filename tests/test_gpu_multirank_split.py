@@ -34,7 +34,7 @@ def _rel(a, b):
 
 @pytest.mark.timeout(300)
 @pytest.mark.parametrize("G,M,method", [(2, 8, "proj_qr"), (3, 5, "proj_qr"), (2, 30, "proj_qr"),
-                                        (4, 3, "proj_classic")])
+                                        (4, 3, "proj_classic"), (8, 8, "proj_qr")])
 def test_split_schedule_with_in_process_ranks_matches_unsharded_oracle(G, M, method):
     from paper_2009_10863_b200 import (InitialGuess, ig_comm_create_local, ig_comm_destroy, ig_copy_history,
                                        ig_local_group_create, ig_local_group_destroy, shard_range)

@@ -28,8 +28,9 @@ def _lib():
 
 @pytest.mark.timeout(300)
 @pytest.mark.parametrize("G,M,method", [(2, 8, "proj_qr"), (3, 5, "proj_qr"), (2, 30, "proj_qr"), (4, 3, "proj_qr"),
-                                         (2, 4, "proj_classic")])
+                                         (2, 4, "proj_classic"), (8, 8, "proj_qr"), (8, 4, "proj_classic")])
 def test_virtual_ranks_match_unsharded_oracle(G, M, method):
+    """G = 8 is the largest exchange (MAXG, one 8-GPU NVLink node): every window slot and flag."""
     from paper_2009_10863_b200 import InitialGuess, attach_virtual_ranks, ig_set_grid_limit, shard_range
 
     g = Grid(41, 2)  # N = 1681: odd shards
