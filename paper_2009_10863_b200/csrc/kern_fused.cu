@@ -317,15 +317,11 @@ __global__ void __launch_bounds__(THREADS, 1) k_update_fused(ProjArgs a) {
             while ((int64_t)q < nq + nh) {
                 unsigned qn = (lane == 0) ? atomicAdd(&c->dyn3[e & 1], 1u) : 0u;  // claim the next one early
                 U3Trip<MC, U3, V> r;
-                if ((int64_t)q < nq) {
-                    const int64_t i0 = S + (int64_t)q * WCH + lane;
-                    u3trip_load(r, a, i0, 32, nv, deff, pend, adm, pol.stream);
-                    u3trip_store(r, a, i0, 32, nv, deff, pend, adm, inv, c1, c2, gc, gs, pol.stream);
-                } else {
-                    const int64_t i0 = ((int64_t)q - nq) * chunk + lane;
-                    u3trip_load(r, a, i0, stride, nv, deff, pend, adm, pol.stream);
-                    u3trip_store(r, a, i0, stride, nv, deff, pend, adm, inv, c1, c2, gc, gs, pol.stream);
-                }
+                const bool tchunk = (int64_t)q < nq;  // one copy of the trip code for both kinds
+                const int64_t i0 = tchunk ? S + (int64_t)q * WCH + lane : ((int64_t)q - nq) * chunk + lane;
+                const int64_t st = tchunk ? 32 : stride;
+                u3trip_load(r, a, i0, st, nv, deff, pend, adm, pol.stream);
+                u3trip_store(r, a, i0, st, nv, deff, pend, adm, inv, c1, c2, gc, gs, pol.stream);
                 q = __shfl_sync(0xffffffffu, qn, 0);
             }
         }
