@@ -223,11 +223,9 @@ __global__ void __launch_bounds__(THREADS, 1) k_update_fused(ProjArgs a) {
     if (deff > 0) {
 #pragma unroll
         for (int k = 0; k <= MC; ++k) v[k] = 0.0;
-        if (ntrip2 > 0) u2trip_compute(pre2, c1, v);
-        for (int64_t t = ntrip2 - 2; t >= 0; --t) {
-            U2Trip<MC, UB, V> r;
-            u2trip_load(r, a, i_first + t * UB * stride, stride, nv, deff, pol.keep);
-            u2trip_compute(r, c1, v);
+        for (int64_t t = ntrip2 - 1; t >= 0; --t) {  // one copy of the trip code (pre2 = the first)
+            if (t < ntrip2 - 1) u2trip_load(pre2, a, i_first + t * UB * stride, stride, nv, deff, pol.keep);
+            u2trip_compute(pre2, c1, v);
         }
         if (tail) {
             U2Trip<MC, 1, double> r;
