@@ -37,4 +37,35 @@ for method, cls in (("extrap_ls", ExtrapLS), ("extrap_sparse", ExtrapSparse)):
             ig.update(torch.from_numpy(x).cuda())
         ig.close()
         print(method, M, p, "ok", flush=True)
+# multi-trip size (360,000 DOFs): the dynamically claimed pass-3 tail, the Givens planner's
+# handed-off trips, the launch-epoch barrier counters; batch and host-buffer batch calls
+from paper_2009_10863_b200 import ig_form_guess_batch, ig_form_guess_batch_host, ig_update_batch, ig_update_batch_host
+
+gb = Grid(600, 2)
+ora_q, ora_e = ProjQR(gb.N, 8), ExtrapLS(gb.N, 8, 3)
+hq, he = InitialGuess(gb.N, "proj_qr", 8), InitialGuess(gb.N, "extrap_ls", 8, 3)
+worst = 0.0
+for n in range(12):
+    b, x, Ax = (t.numpy() for t in manufactured_step(gb, n, dt=1e-2))
+    if n % 2 == 0:
+        x0s = [torch.zeros(gb.N, dtype=torch.float64, device="cuda") for _ in range(2)]
+        ig_form_guess_batch([hq, he], [torch.from_numpy(b).cuda(), None], x0s)
+        got = [t.cpu().numpy() for t in x0s]
+    else:
+        x0s = [torch.zeros(gb.N, dtype=torch.float64).pin_memory() for _ in range(2)]
+        ig_form_guess_batch_host([hq, he], [torch.from_numpy(b).pin_memory(), None], x0s)
+        got = [t.numpy() for t in x0s]
+    for o, gval in zip((ora_q, ora_e), got):
+        ref = o.form_guess(b, np.zeros(gb.N))
+        worst = max(worst, np.linalg.norm(gval - ref) / max(np.linalg.norm(ref), 1e-300))
+    ora_q.update(x, Ax)
+    ora_e.update(x)
+    if n % 2 == 0:
+        ig_update_batch([hq, he], [torch.from_numpy(x).cuda()] * 2, [torch.from_numpy(Ax).cuda(), None])
+    else:
+        ig_update_batch_host([hq, he], [torch.from_numpy(x).pin_memory()] * 2, [torch.from_numpy(Ax).pin_memory(), None])
+hq.close()
+he.close()
+print("multi-trip batch", f"{worst:.1e}", flush=True)
+assert worst < 1e-11
 print("SANITIZE RUN OK")
