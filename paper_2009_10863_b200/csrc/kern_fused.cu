@@ -35,6 +35,10 @@ extern "C" int ig_debug_trace_read_form(unsigned long long *host, int n) {
 #define TRACE_F(slot) do { } while (0)
 #endif
 
+#ifndef IG_UP1_MC8
+#define IG_UP1_MC8 3  // form pass-1 unroll at M = 8 (A/B: 2 -> 208.1, 3 -> 207.8, 4 -> 208.0 us/step at C2)
+#endif
+
 namespace ig {
 
 // Second block-partial buffer so that a fast CTA's pass-2 partials never overwrite pass-1
@@ -68,14 +72,15 @@ __global__ void __launch_bounds__(THREADS, 1) k_form_fused(ProjArgs a) {
     const int64_t nv = a.N / VEC;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     const int64_t i_first = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    // ---- pass 1: alpha = B~^T b
+    // ---- pass 1: alpha = B~^T b (UP strided elements per trip: read-only, more bytes in flight)
+    constexpr int UP = (MC == 8) ? IG_UP1_MC8 : U;
     double v[MC + 1];
 #pragma unroll
     for (int k = 0; k <= MC; ++k) v[k] = 0.0;
-    for (int64_t i0 = i_first; i0 < nv; i0 += U * stride) {
-        V bv[U], col[U][MC];
+    for (int64_t i0 = i_first; i0 < nv; i0 += UP * stride) {
+        V bv[UP], col[UP][MC];
 #pragma unroll
-        for (int u = 0; u < U; ++u) {
+        for (int u = 0; u < UP; ++u) {
             const int64_t i = i0 + u * stride;
             const bool ok = i < nv;
             bv[u] = ok ? ldp<V>(a.b, i, ps) : vzero(V());
@@ -83,7 +88,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_form_fused(ProjArgs a) {
             for (int k = 0; k < MC; ++k) col[u][k] = (ok && k < d) ? ldp<V>(a.Bt + k * a.ld, i, ps) : vzero(V());
         }
 #pragma unroll
-        for (int u = 0; u < U; ++u)
+        for (int u = 0; u < UP; ++u)
 #pragma unroll
             for (int k = 0; k < MC; ++k) v[k] = vdot(col[u][k], bv[u], v[k]);
     }
