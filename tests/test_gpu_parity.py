@@ -272,6 +272,28 @@ def test_host_entry_points_match_oracle():
     he.close()
 
 
+def test_host_entry_points_accept_pageable_memory():
+    """The host-buffer calls also take ordinary (pageable) host arrays -- slower transfers, same
+    results as pinned buffers."""
+    from paper_2009_10863_b200 import InitialGuess, ig_form_guess_batch_host, ig_update_batch_host
+
+    g = Grid(20, 2)
+    seq = _seq(g, 8, dt=1e-2)
+    A = [InitialGuess(g.N, "proj_qr", 4), InitialGuess(g.N, "extrap_ls", 4, 2)]
+    B = [InitialGuess(g.N, "proj_qr", 4), InitialGuess(g.N, "extrap_ls", 4, 2)]
+    for b, x, Ax in seq:
+        xa = [torch.zeros(g.N, dtype=torch.float64) for _ in A]  # pageable
+        xb = [torch.zeros(g.N, dtype=torch.float64).pin_memory() for _ in B]
+        ig_form_guess_batch_host(A, [torch.from_numpy(b.copy()), None], xa)
+        ig_form_guess_batch_host(B, [torch.from_numpy(b).pin_memory(), None], xb)
+        for u, v in zip(xa, xb):
+            assert torch.equal(u, v)
+        ig_update_batch_host(A, [torch.from_numpy(x.copy())] * 2, [torch.from_numpy(Ax.copy()), None])
+        ig_update_batch_host(B, [torch.from_numpy(x).pin_memory()] * 2, [torch.from_numpy(Ax).pin_memory(), None])
+    for h in A + B:
+        h.close()
+
+
 def test_batch_host_entry_points_match_single_calls_and_oracle():
     """ig_form_guess_batch_host / ig_update_batch_host (transfers of the fields overlapped on two
     streams per handle) against the device-buffer single calls on twin handles, bitwise, and the
