@@ -35,6 +35,12 @@ extern "C" int ig_debug_trace_read_form(unsigned long long *host, int n) {
 #define TRACE_F(slot) do { } while (0)
 #endif
 
+#ifndef IG_UU1_MC8
+#define IG_UU1_MC8 2  // update pass-1 elements per trip at M = 8 (A/B knob)
+#endif
+#ifndef IG_FP_MC8
+#define IG_FP_MC8 2  // form pass-2 trips prefetched across the barrier at M <= 8 (A/B knob)
+#endif
 #ifndef IG_UP1_MC8
 #define IG_UP1_MC8 3  // form pass-1 unroll at M = 8 (A/B: 2 -> 208.1, 3 -> 207.8, 4 -> 208.0 us/step at C2)
 #endif
@@ -101,7 +107,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_form_fused(ProjArgs a) {
     }
     // the first FP trips of pass 2 are in flight across the barrier (the bubble is ~2-4 us: one
     // trip of 1 CTA/SM covers ~1.5 us of the SM's bandwidth share)
-    constexpr int FP = (MC <= 8) ? 2 : 1;
+    constexpr int FP = (MC <= 8) ? IG_FP_MC8 : 1;
     XTrip<MC, U, V> pre[FP];
 #pragma unroll
     for (int f = 0; f < FP; ++f) xtrip_load(pre[f], a, i_first + f * U * stride, stride, nv, d, ps);
@@ -201,7 +207,8 @@ __global__ void __launch_bounds__(THREADS, 1) k_update_fused(ProjArgs a) {
     double v[MC + 1];
 #pragma unroll
     for (int k = 0; k <= MC; ++k) v[k] = 0.0;
-    for (int64_t i0 = i_first; i0 < nv; i0 += U * stride) u1_trip<MC, U, V>(a, i0, stride, nv, pend, deff, gc, gs, v, pol.keep);
+    constexpr int UU1 = (MC == 8) ? IG_UU1_MC8 : U;  // pass-1 elements per trip (A/B knob)
+    for (int64_t i0 = i_first; i0 < nv; i0 += UU1 * stride) u1_trip<MC, UU1, V>(a, i0, stride, nv, pend, deff, gc, gs, v, pol.keep);
     if (tail) u1_trip<MC, 1, double>(a, a.N - 1, 1, a.N, pend, deff, gc, gs, v, pol.keep);
     // Serpentine order: pass 2 walks the vectors BACKWARDS, so it starts on the B~/Ax lines pass 1
     // touched last (still in the 126 MB L2); pass 3 walks forwards again and starts on what pass 2
