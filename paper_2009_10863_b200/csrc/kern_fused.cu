@@ -9,9 +9,13 @@
 //
 //   k_form_fused   : [alpha = B~^T b] --barrier--> [x0 = X~ alpha]
 //   k_update_fused : [B~ downdate + c1, ||Ax||^2] --barrier--> [c2, ||b1||^2] --barrier-->
-//                    [X~ downdate + x~, b~, admission, new columns] --exit--> control block
-// The element arithmetic is the same device code as the one-kernel-per-pass path
-// (proj_common.cuh), which stays in use when partial sums must cross ranks (G > 1).
+//                    [X~ downdate + x~, b~, admission, new columns; warp 0 of CTA 0: R update and
+//                    the next downdate's Givens plan, its trips claimed by the others]
+//                    --> CTA 0 writes the control block (no exit barrier)
+// Barrier and claim counters are double-buffered by a launch epoch in the control block.  The
+// element arithmetic is the same device code as the one-kernel-per-pass path (proj_common.cuh),
+// which stays in use when partial sums cross ranks through an all-gather (ig_attach_comm); with
+// the in-kernel peer exchange (ig_attach_peers) these kernels are used for G > 1 as well.
 #include <cstdlib>
 #include <type_traits>
 
