@@ -12,7 +12,10 @@ timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:'
    --log-file gpurun_out/launches.csv python bench.py --steps 4 --warmup 40 --e2e-steps 1 --no-cpu-baseline > gpurun_out/ncu_launch.log 2>&1
 KREGEX="k_update_fused|k_form_fused|k_extrap|k_copy" SKIP=40 COUNT=4 bash scripts/ncu_full.sh
 python scripts/summarize_ncu.py --launches gpurun_out/launches.csv --full gpurun_out/prof.ncu-rep --bench gpurun_out/bench.log --tag ${TAG} > gpurun_out/summary.log 2>&1
-cp -r profiles gpurun_out/profiles_new
+# only this tag's files travel back (gpurun_out is capped at 64 MiB)
+mkdir -p gpurun_out/profiles_new
+cp profiles/${TAG}_* profiles/traffic.json gpurun_out/profiles_new/ 2>/dev/null
+rm -f gpurun_out/prof.ncu-rep
 for f in pytest_gpu smoke bench bench_ref; do tail -n 2 gpurun_out/$f.log; done
 timeout 1200 python scripts/bench_sweep.py --out gpurun_out/profiles_new/${TAG}_sweep.md > gpurun_out/sweep.log 2>&1
 bash scripts/sanitize.sh > gpurun_out/sanitize_summary.txt 2>&1
