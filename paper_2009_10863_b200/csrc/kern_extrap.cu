@@ -109,10 +109,13 @@ template <class K> static int grid_for_x(K kern, int64_t nv, int nsm) {
     return (int)g;
 }
 
+#ifndef IG_EXU8
+#define IG_EXU8 2  // elements per trip of the 8-term extrapolation combine (A/B on C2: 1 -> 207.8, 2 -> 207.4 us/step)
+#endif
 template <int FC>
 static void launch_fc(const ExtrapArgs &a, int vec, int nsm, cudaStream_t s) {
     if (vec == 2) {
-        constexpr int U = FC <= 2 ? 4 : (FC <= 4 ? 2 : 1);
+        constexpr int U = FC <= 2 ? 4 : (FC <= 4 ? 2 : (FC == 8 ? IG_EXU8 : 1));
         auto k = k_extrap<FC, 2, U>;  // U strided elements per trip when few streams
         launch_ex(k, grid_for_x(k, a.N / 2, nsm), s, false, a);
     } else {
