@@ -21,7 +21,7 @@ LIB = os.path.join(PKG, "libig.so")
 SOURCES = ["kern_proj.cu", "kern_fused.cu", "kern_extrap.cu", "coeffs.cpp", "api.cpp"]
 HEADERS = [os.path.join(CSRC, "ig_internal.h"), os.path.join(CSRC, "proj_common.cuh"), os.path.join(INCLUDE, "ig.h")]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-FLAGS = [*(["-DIG_U2_MC8=" + os.environ["IG_U2_MC8"]] if os.environ.get("IG_U2_MC8") else []), *(["-DIG_UP1_MC8=" + os.environ["IG_UP1_MC8"]] if os.environ.get("IG_UP1_MC8") else []), *(["-DIG_UU1_MC8=" + os.environ["IG_UU1_MC8"]] if os.environ.get("IG_UU1_MC8") else []), *(["-DIG_FP_MC8=" + os.environ["IG_FP_MC8"]] if os.environ.get("IG_FP_MC8") else []), *(["-DIG_EXU8=" + os.environ["IG_EXU8"]] if os.environ.get("IG_EXU8") else []), *(["-DIG_TRACE=1"] if os.environ.get("IG_TRACE") else []), "-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xptxas", "-v", f"-I{INCLUDE}", f"-I{CSRC}"]
+FLAGS = [*(["-DIG_U2_MC8=" + os.environ["IG_U2_MC8"]] if os.environ.get("IG_U2_MC8") else []), *(["-DIG_UP1_MC8=" + os.environ["IG_UP1_MC8"]] if os.environ.get("IG_UP1_MC8") else []), *(["-DIG_UU1_MC8=" + os.environ["IG_UU1_MC8"]] if os.environ.get("IG_UU1_MC8") else []), *(["-DIG_FP_MC8=" + os.environ["IG_FP_MC8"]] if os.environ.get("IG_FP_MC8") else []), *(["-DIG_EXU8=" + os.environ["IG_EXU8"]] if os.environ.get("IG_EXU8") else []), *(["-DIG_UX_MC8=" + os.environ["IG_UX_MC8"]] if os.environ.get("IG_UX_MC8") else []), *(["-DIG_TRACE=1"] if os.environ.get("IG_TRACE") else []), "-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xptxas", "-v", f"-I{INCLUDE}", f"-I{CSRC}"]
 
 
 def _nvcc() -> str:

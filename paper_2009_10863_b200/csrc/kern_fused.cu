@@ -43,7 +43,10 @@ extern "C" int ig_debug_trace_read_form(unsigned long long *host, int n) {
 #define IG_UU1_MC8 2  // update pass-1 elements per trip at M = 8 (A/B knob)
 #endif
 #ifndef IG_FP_MC8
-#define IG_FP_MC8 2  // form pass-2 trips prefetched across the barrier at M <= 8 (A/B knob)
+#define IG_FP_MC8 1  // form pass-2 trips prefetched across the barrier at M = 8 (A/B knob, with IG_UX_MC8)
+#endif
+#ifndef IG_UX_MC8
+#define IG_UX_MC8 3  // form pass-2 elements per trip at M = 8 (A/B: 2x2 prefetched 207.4, 3x1 207.2, 4x1 207.8, 1x4 212.2 us)
 #endif
 #ifndef IG_UP1_MC8
 #define IG_UP1_MC8 3  // form pass-1 unroll at M = 8 (A/B: 2 -> 208.1, 3 -> 207.8, 4 -> 208.0 us/step at C2)
@@ -111,10 +114,11 @@ __global__ void __launch_bounds__(THREADS, 1) k_form_fused(ProjArgs a) {
     }
     // the first FP trips of pass 2 are in flight across the barrier (the bubble is ~2-4 us: one
     // trip of 1 CTA/SM covers ~1.5 us of the SM's bandwidth share)
-    constexpr int FP = (MC <= 8) ? IG_FP_MC8 : 1;
-    XTrip<MC, U, V> pre[FP];
+    constexpr int FP = (MC == 8) ? IG_FP_MC8 : ((MC < 8) ? 2 : 1);
+    constexpr int UX = (MC == 8) ? IG_UX_MC8 : U;  // pass-2 elements per trip (A/B knob)
+    XTrip<MC, UX, V> pre[FP];
 #pragma unroll
-    for (int f = 0; f < FP; ++f) xtrip_load(pre[f], a, i_first + f * U * stride, stride, nv, d, ps);
+    for (int f = 0; f < FP; ++f) xtrip_load(pre[f], a, i_first + f * UX * stride, stride, nv, d, ps);
     block_partials_store<MC + 1>(v, d, false, a.blk, sh);
     TRACE_F(1);
     grid_barrier(&c->bar[e & 1], 1, &c->err, a.watchdog_ns);
@@ -128,9 +132,9 @@ __global__ void __launch_bounds__(THREADS, 1) k_form_fused(ProjArgs a) {
     for (int k = 0; k < MC; ++k) al[k] = (k < d) ? s_red[k] : 0.0;
     // ---- pass 2: x0 = X~ alpha (b fully consumed before the barrier: x0 may alias b)
 #pragma unroll
-    for (int f = 0; f < FP; ++f) xtrip_store(pre[f], a, i_first + f * U * stride, stride, nv, al);
-    for (int64_t i0 = i_first + FP * U * stride; i0 < nv; i0 += U * stride) {
-        XTrip<MC, U, V> r;
+    for (int f = 0; f < FP; ++f) xtrip_store(pre[f], a, i_first + f * UX * stride, stride, nv, al);
+    for (int64_t i0 = i_first + FP * UX * stride; i0 < nv; i0 += UX * stride) {
+        XTrip<MC, UX, V> r;
         xtrip_load(r, a, i0, stride, nv, d, ps);
         xtrip_store(r, a, i0, stride, nv, al);
     }
