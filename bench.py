@@ -1,20 +1,30 @@
 #!/usr/bin/env python
 """bench.py -- initial-guess form+update throughput on B200 (arXiv 2009.10863 hot path).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config c3|c2|c4]
+                    [--scaling weak|strong] [--dry-run]
     torchrun --nproc-per-node N --master-addr 127.0.0.1 ... bench.py --gpus N ...
 
-Workload (BASELINE.json configs[1], "C2"): 3D 128^3 7-point Helmholtz manufactured sequence
-(2,097,152 fp64 DOFs per GPU), projection QR(8) and extrapolation EXTRAP(3,8) on the same
-time steps.  One STEP = the whole hot path once: QR form + QR update + EXTRAP form + EXTRAP
-update (push by copy) on that step's fresh (b_n, x_n, A x_n), all resident in HBM.
-With N > 1 every rank holds a contiguous z-slab of 128^3 DOFs of a 128x128x(128N) global
-problem (weak scaling); the projection's global sums go through the in-kernel NVLink peer
-exchange (--exchange peer, default; NCCL all-gather between kernels with --exchange nccl or when
-the GPUs lack P2P), extrapolation never communicates.  --config c3|c4 selects configs[2]/[3].
+Headline workload (BASELINE.json configs[2], "C3", the configuration the metric is quoted on):
+3D 512^3 7-point Poisson-like manufactured sequence, 2^27 = 134,217,728 fp64 DOFs per GPU,
+projection QR(8) and extrapolation EXTRAP(3,8) on the same time steps.  One STEP = the whole hot
+path once: QR form + QR update + EXTRAP form + EXTRAP update (push by copy) on that step's
+(b_n, x_n, A x_n), all resident in HBM (1.07 GB vectors: every stream is an HBM stream, no L2
+reuse between steps).  The line also carries the configs[1] point ("C2", 128^3 = 2^21 DOFs) under
+"c2_l2_assisted": at 16.8 MB per vector L2 serves part of the update's re-reads, so that point is
+NOT an HBM measurement (N < 2^24).  --config c4 selects configs[3] (2^28 DOFs/GPU,
+QR(16)+EXTRAP(3,16)).
+
+Scaling (N > 1 ranks, one per GPU): --scaling weak (default) gives every rank its own z-slab of
+the config's size (global grid n x n x (nz*N)); --scaling strong splits the config's FIXED global
+grid into N contiguous z-plane ranges (shard_range; sizes differ by at most one plane), so t(N)
+can be compared with t(1): E(N) = t(1)/(N t(N)) (--t1-ms, or computed by the driver).  The
+projection's global sums go through the in-kernel NVLink peer exchange (--exchange peer, default;
+NCCL all-gather between kernels with --exchange nccl or when the GPUs lack P2P); extrapolation
+never communicates.  --dry-run: no GPU work, prints the partition plan (CPU tests).
 
 value = effective HBM GB/s of the whole job = (algorithmic bytes of all ranks) / (max-over-ranks
-device time), algorithmic bytes per step and rank = [(8M+4) + (nnz(beta)+1) + 2] * 8 * N
+device time), algorithmic bytes per step and rank = [(8M+4) + (nnz(beta)+1) + 2] * 8 * N_rank
 (DESIGN.md section 7).  ms_per_step is reported beside it.  Also on the JSON line: roofline (the
 dominant kernel against the measured copy peak, plus read-only and nominal ceilings), kernels
 (per-kernel event timing from a second pass), step_stats, fill_phase, clocks, e2e (host-buffer
@@ -46,9 +56,14 @@ def parse():
     p.add_argument("--steps", type=int, default=200)
     p.add_argument("--warmup", type=int, default=10)
     p.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    p.add_argument("--config", choices=["c2", "c3", "c4"], default="c2",
-                   help="c2 (default): configs[1] 128^3 QR(8)+EXTRAP(3,8); c3: configs[2] 512^3 (2^27 DOFs) QR(m); "
-                        "c4: configs[3] 2^28 DOFs/GPU QR(16)+EXTRAP(3,16)")
+    p.add_argument("--config", choices=["c2", "c3", "c4"], default="c3",
+                   help="c3 (default): configs[2] 512^3 (2^27 DOFs) QR(8)+EXTRAP(3,8); c2: configs[1] 128^3 "
+                        "(L2-assisted); c4: configs[3] 2^28 DOFs/GPU QR(16)+EXTRAP(3,16)")
+    p.add_argument("--scaling", choices=["weak", "strong"], default="weak",
+                   help="N>1: weak = a config-sized slab per rank; strong = the config's global grid split in z-slabs")
+    p.add_argument("--t1-ms", type=float, default=None, help="strong scaling: t(1) in ms/step for E(N) = t(1)/(N t(N))")
+    p.add_argument("--dry-run", action="store_true", help="no GPU work: print the partition plan (CPU tests)")
+    p.add_argument("--no-c2", action="store_true", help="skip the extra C2 (L2-assisted) point of the default run")
     p.add_argument("--n", type=int, default=None, help="grid points per direction (per-GPU slab n^3), overrides --config")
     p.add_argument("--m", type=int, default=None, help="history size M (projection and extrapolation)")
     p.add_argument("--degree", type=int, default=3, help="extrapolation degree")
@@ -71,6 +86,23 @@ def parse():
         a.m = shape[3]
     a.cfg_name = {"c2": "C2 configs[1]", "c3": "C3 configs[2]", "c4": "C4 configs[3]"}[a.config]
     return a
+
+
+def partition(args, world: int, rank: int):
+    """(nz_global, z0, z1): this rank's contiguous z-plane range (SURVEY §8(e) DOF shards)."""
+    from paper_2009_10863_b200.ig import shard_range
+
+    if args.scaling == "weak":  # every rank holds args.nz planes of an n x n x (nz*world) grid
+        return args.nz * world, rank * args.nz, (rank + 1) * args.nz
+    lo, hi = shard_range(args.nz, world, rank)  # the fixed n x n x nz grid, planes split evenly
+    if hi <= lo:
+        raise SystemExit(f"--scaling strong: {args.nz} z-planes cannot be split over {world} ranks")
+    return args.nz, lo, hi
+
+
+def l2_label(N: int) -> str | None:
+    """per-vector sizes below 2^24 doubles are partly served by the 126 MB L2."""
+    return "L2-assisted (N < 2^24), not an HBM measurement" if N < (1 << 24) else None
 
 
 def peak_hbm():
@@ -268,7 +300,11 @@ def run_reference(args, world, rank):
         return
     n, M, p = args.nxy, args.m, args.degree
     N_full = n * n * args.nz
-    nz = max(1, (1 << 18) // (n * n))  # a ~262K-DOF contiguous z-slab sample of the workload
+    # the same contiguous z-slab sample as our arm's cpu_baseline (2^21 DOFs, 8 planes at C3), thinned
+    # only when K is large so the whole --steps K --warmup W run stays within a few minutes
+    nz = max(1, min(args.nz, (1 << 21) // (n * n)))
+    if args.steps > 200:
+        nz = max(1, nz * 200 // args.steps)
     # warm-up steps double as history fill; each timed step is one oracle step on the sample
     sps, bps, done, Ns = oracle_sample_run(n, M, p, nz, args.steps, None, max(args.warmup, M + 1))
     gbs = bps / sps / 1e9
@@ -286,17 +322,21 @@ def run_reference(args, world, rank):
 
 
 # ------------------------------------------------------------------------------------------ our arm
-def run_ours(args, world, rank, local):
+def measure(args, world, rank, local, full: bool):
+    """Time K steps of the hot path on this rank's slab; returns the JSON fields of one config.
+    full=False (the extra C2 point): headline value, kernels and roofline only."""
     import torch
 
     from paper_2009_10863_b200 import (InitialGuess, comm_from_process_group, ig_form_guess_batch_host,
                                        ig_form_guess_host, ig_profile, ig_profile_read, ig_total_launches,
                                        ig_update_batch_host, ig_update_host, peers_from_process_group)
-    from workloads.gen import manufactured_step_slab
+    from workloads.gen import manufactured_step_zrange
 
     n, M, p = args.nxy, args.m, args.degree
-    nz = args.nz
+    nzg, z0, z1 = partition(args, world, rank)
+    nz = z1 - z0
     N = n * n * nz
+    N_total = n * n * (nzg if args.scaling == "strong" else args.nz * world)
     K, W = args.steps, args.warmup
     prefill = max(0, M + 1 - W)  # untimed history fill when W is too short to reach the steady state
     S = prefill + W + K
@@ -317,8 +357,12 @@ def run_ours(args, world, rank, local):
         # fits.  Inputs are regenerated into fixed buffers between steps, OUTSIDE the timed
         # windows: every step is bracketed by its own events and the K windows are summed.
         P, regen = 1, True
-    ro_gbs = read_only_ceiling(dev) if rank == 0 else None
-    pool = [manufactured_step_slab(n, nz, rank, world, k, device=dev) for k in range(P)]
+    ro_gbs = read_only_ceiling(dev) if (rank == 0 and full) else None
+
+    def gen(k):
+        return manufactured_step_zrange(n, nzg, z0, z1, k, device=dev)
+
+    pool = [gen(k) for k in range(P)]
     torch.cuda.synchronize()
 
     comm = comm_from_process_group() if (world > 1 and args.exchange == "nccl") else None
@@ -330,17 +374,22 @@ def run_ours(args, world, rank, local):
             ig_set_grid_limit(hp.h, torch.cuda.get_device_properties(dev).multi_processor_count // world)
         try:
             peers_from_process_group([hp.h])
+            print(f"[bench] rank {rank}/{world}: in-kernel peer exchange attached (CUDA IPC windows of "
+                  f"{world} ranks, NVLink P2P), {N} DOFs = z-planes [{z0}, {z1}) of {nzg}", file=sys.stderr, flush=True)
         except RuntimeError as e:  # no P2P between the GPUs: fall back to NCCL between kernels
             print(f"[bench] peer exchange unavailable ({e}); using NCCL", file=sys.stderr, flush=True)
             args.exchange = "nccl"
             hp.close()
             hp = InitialGuess(N, "proj_qr", M, comm=comm_from_process_group())
+    if world > 1 and args.exchange == "nccl":
+        print(f"[bench] rank {rank}/{world}: NCCL communicator attached, {N} DOFs = z-planes [{z0}, {z1}) of {nzg}",
+              file=sys.stderr, flush=True)
     he = InitialGuess(N, "extrap_ls", M, p)
     x0p = torch.zeros(N, dtype=torch.float64, device=dev)
     x0e = torch.zeros(N, dtype=torch.float64, device=dev)
 
     def refill(k):  # regen mode: step k's inputs into the single pool slot (untimed)
-        for dst, src in zip(pool[0], manufactured_step_slab(n, nz, rank, world, k, device=dev)):
+        for dst, src in zip(pool[0], gen(k)):
             dst.copy_(src)
             del src
 
@@ -400,8 +449,10 @@ def run_ours(args, world, rank, local):
     assert efb + eub == eb, f"library extrapolation byte count {efb + eub} != analytic {eb}"
     assert st["admitted"] == 1
 
-    step_bytes = pb + eb
-    value = world * step_bytes * K / (t_ms * 1e-3) / 1e9
+    step_bytes = pb + eb  # this rank's
+    pbT, ebT, _ = bytes_per_step(M, N_total, nnz)
+    job_bytes = pbT + ebT  # all ranks (bytes are linear in the slab length)
+    value = job_bytes * K / (t_ms * 1e-3) / 1e9
     ms_per_step = t_ms / K
 
     # ---- per-kernel CUDA-event timing over a second K-step pass (same inputs, cycled)
@@ -435,16 +486,28 @@ def run_ours(args, world, rank, local):
                 tj = json.load(f)
             key = f"{dom}@M{M}N{N}"
             if key in tj:
-                traffic, traffic_src = tj[key], "profiles/traffic.json (ncu --set full dram__bytes_read+write)"
+                traffic = tj[key]
+                src = tj.get("_source", {}).get(key, "ncu --set full")
+                traffic_src = f"profiles/traffic.json[{key}] (dram__bytes_read.sum + dram__bytes_write.sum, {src})"
         except Exception:
             pass
     roofline = {"bound": "hbm", "kernel": f"k_{dom}", "achieved": kernels[dom]["gbs"], "peak": peak, "unit": "GB/s",
                 "frac": kernels[dom]["gbs"] / peak, "traffic": traffic, "peak_source": peak_src,
                 "algorithmic_bytes_per_launch": per_kernel[dom], "traffic_source": traffic_src,
+                "traffic_over_algorithmic": (traffic / per_kernel[dom]) if traffic else None,
                 "step_frac": (step_bytes / (ms_per_step * 1e-3) / 1e9) / peak,
-                "frac_nominal": kernels[dom]["gbs"] / NOMINAL_HBM,
-                "ceilings_gbs": {"copy_measured": peak, "read_only_measured": ro_gbs, "nominal": NOMINAL_HBM,
-                                 "read_only_how": "torch.sum over 2^28 fp64 (2.1 GB), best of 5, CUDA events"}}
+                "frac_nominal": kernels[dom]["gbs"] / NOMINAL_HBM}
+    if full:
+        roofline["ceilings_gbs"] = {"copy_measured": peak, "read_only_measured": ro_gbs, "nominal": NOMINAL_HBM,
+                                    "read_only_how": "torch.sum over 2^28 fp64 (2.1 GB), best of 5, CUDA events"}
+    res = {"value": value, "ms_per_step": ms_per_step, "N": N, "N_total": N_total, "z": (z0, z1, nzg), "M": M,
+           "p": p, "nnz": nnz, "P": P, "regen": regen, "prefill": prefill, "step_bytes": step_bytes,
+           "launches": launches, "roofline": roofline, "kernels": kernels, "clocks": sampler.summary(),
+           "proj_state": {"d": st["d"], "rho_last": st["rho"]}, "host_us": host_us}
+    if not full:
+        hp.close()
+        he.close()
+        return res
 
     # ---- per-step distribution: a third pass with an event between consecutive steps (regen
     # mode: the headline's own per-step windows)
@@ -457,16 +520,16 @@ def run_ours(args, world, rank, local):
         torch.cuda.synchronize()
         step_ms = [evs[j].elapsed_time(evs[j + 1]) for j in range(K)]
     q = statistics.quantiles(step_ms, n=10) if len(step_ms) >= 2 else [step_ms[0]] * 9
-    step_stats = {"median_us": statistics.median(step_ms) * 1e3, "p10_us": q[0] * 1e3, "p90_us": q[-1] * 1e3,
-                  "steps": len(step_ms), "how": "per-step CUDA events (separate pass)" if not regen
-                  else "the headline's per-step windows"}
+    res["step_stats"] = {"median_us": statistics.median(step_ms) * 1e3, "p10_us": q[0] * 1e3, "p90_us": q[-1] * 1e3,
+                         "steps": len(step_ms), "how": "per-step CUDA events (separate pass)" if not regen
+                         else "the headline's per-step windows"}
 
     # ---- end to end through the public host-buffer API (H2D of inputs and D2H of guesses timed)
     # M+1 distinct host steps: a pair re-enters only after it left the M-window (admission path)
     PH = M + 1
-    if regen or PH > len(pool) or 3 * PH * vec_gb > 32.0:
-        e2e = {"value": None, "unit": "GB/s", "h2d_bytes_per_step": 4 * 8 * N, "d2h_bytes_per_step": 2 * 8 * N,
-               "unavailable": "M+1 distinct pinned host input steps (to stay on the admission path) exceed 32 GB"}
+    if regen or PH > len(pool) or 3 * PH * vec_gb > 40.0:
+        res["e2e"] = {"value": None, "unit": "GB/s", "h2d_bytes_per_step": 4 * 8 * N, "d2h_bytes_per_step": 2 * 8 * N,
+                      "unavailable": "M+1 distinct pinned host input steps (to stay on the admission path) exceed 40 GB"}
     else:
         host = [tuple(t.cpu().pin_memory() for t in pool[(prefill + W + j) % len(pool)]) for j in range(PH)]
         x0h_p = torch.zeros(N, dtype=torch.float64).pin_memory()
@@ -496,17 +559,18 @@ def run_ours(args, world, rank, local):
 
         te1 = e2e_run(False)
         te = e2e_run(True)
-        e2e = {"value": world * step_bytes * KE / te / 1e9, "unit": "GB/s", "ms_per_step": te / KE * 1e3,
-               "h2d_bytes_per_step": 4 * 8 * N, "d2h_bytes_per_step": 2 * 8 * N, "steps": KE,
-               "h2d_vectors": "QR: b, x, Ax (the fallback x0 is not uploaded once d > 0); EXTRAP: x",
-               "api": "ig_form_guess_batch_host/ig_update_batch_host (pinned host buffers, one call per "
-                      "time step for both fields; transfers of the fields overlap)",
-               "single_calls": {"value": world * step_bytes * KE / te1 / 1e9, "ms_per_step": te1 / KE * 1e3,
-                                "api": "ig_form_guess_host/ig_update_host, one call per field"}}
+        res["e2e"] = {"value": job_bytes * KE / te / 1e9, "unit": "GB/s", "ms_per_step": te / KE * 1e3,
+                      "h2d_bytes_per_step": 4 * 8 * N, "d2h_bytes_per_step": 2 * 8 * N, "steps": KE,
+                      "h2d_vectors": "QR: b, x, Ax (the fallback x0 is not uploaded once d > 0); EXTRAP: x",
+                      "api": "ig_form_guess_batch_host/ig_update_batch_host (pinned host buffers, one call per "
+                             "time step for both fields; transfers of the fields overlap)",
+                      "single_calls": {"value": job_bytes * KE / te1 / 1e9, "ms_per_step": te1 / KE * 1e3,
+                                       "api": "ig_form_guess_host/ig_update_host, one call per field"}}
+        del host
 
     # ---- fill phase (reported separately from the steady state): both histories
     # reset, the first M+1 steps timed one by one (projection d = 0..M, extrapolation fill 0..M)
-    fill = None
+    res["fill_phase"] = None
     if not regen:
         hp.reset()
         he.reset()
@@ -520,49 +584,107 @@ def run_ours(args, world, rank, local):
             f_us.append(e0.elapsed_time(e1) * 1e3)
             (a, b_), (c, d_) = hp.bytes(), he.bytes()
             f_bytes.append(a + b_ + c + d_)
-        fill = {"steps": M + 1, "us_per_step": [round(v, 1) for v in f_us],
-                "gbs_per_step": [round(bb / (u * 1e-6) / 1e9) for bb, u in zip(f_bytes, f_us)],
-                "bytes_per_step": f_bytes, "total_us": sum(f_us)}
-
-    # ---- CPU oracle baseline (rank 0, N=1 only)
-    cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        nz_cpu = n if N <= (1 << 22) else max(1, (1 << 21) // (n * n))  # big configs: a 2M-DOF z-slab sample
-        sps, bps, done, Ns = oracle_sample_run(n, M, p, nz_cpu, 10 ** 6, args.cpu_seconds, M + 1)
-        from threadpoolctl import threadpool_limits
-
-        with threadpool_limits(limits=1):  # the same oracle on one host core
-            sps1, bps1, done1, _ = oracle_sample_run(n, M, p, nz_cpu, 10 ** 6, args.cpu_seconds_1t, M + 1)
-        cpu = {"value": bps / sps / 1e9, "unit": "GB/s", "cores": cpu_cores(), "kind": "oracle",
-               "one_core": {"value": bps1 / sps1 / 1e9, "unit": "GB/s", "cores": 1, "steps": done1},
-               "ms_per_step": sps * 1e3,
-               "sample": f"{Ns} DOFs ({'full grid' if Ns == N else 'z-slab sample'}), {done} steady oracle steps "
-                         f"(QR({M})+EXTRAP({p},{M})) after {M + 1} fill steps, ~{args.cpu_seconds:.0f} s budget"}
-
+        res["fill_phase"] = {"steps": M + 1, "us_per_step": [round(v, 1) for v in f_us],
+                             "gbs_per_step": [round(bb / (u * 1e-6) / 1e9) for bb, u in zip(f_bytes, f_us)],
+                             "bytes_per_step": f_bytes, "total_us": sum(f_us)}
     hp.close()
     he.close()
+    return res
+
+
+def cpu_baseline(args, n, M, p, N):
+    """The CPU oracle (as it stands) on rank 0 at N=1: a bounded z-slab sample of the workload."""
+    nz_cpu = args.nz if N <= (1 << 22) else max(1, (1 << 21) // (n * n))  # big configs: a 2M-DOF z-slab sample
+    sps, bps, done, Ns = oracle_sample_run(n, M, p, nz_cpu, 10 ** 6, args.cpu_seconds, M + 1)
+    from threadpoolctl import threadpool_limits
+
+    with threadpool_limits(limits=1):  # the same oracle on one host core
+        sps1, bps1, done1, _ = oracle_sample_run(n, M, p, nz_cpu, 10 ** 6, args.cpu_seconds_1t, M + 1)
+    return {"value": bps / sps / 1e9, "unit": "GB/s", "cores": cpu_cores(), "kind": "oracle",
+            "one_core": {"value": bps1 / sps1 / 1e9, "unit": "GB/s", "cores": 1, "steps": done1},
+            "ms_per_step": sps * 1e3,
+            "sample": f"{Ns} DOFs ({'full grid' if Ns == N else f'{nz_cpu}-plane z-slab sample of the {n}x{n}x{args.nz} grid'}), "
+                      f"{done} steady oracle steps (QR({M})+EXTRAP({p},{M})) after {M + 1} fill steps, "
+                      f"~{args.cpu_seconds:.0f} s budget; GB/s = the step's algorithmic bytes / oracle time"}
+
+
+def run_ours(args, world, rank, local):
+    import copy
+
+    import torch
+
+    n, M, p = args.nxy, args.m, args.degree
+    r = measure(args, world, rank, local, full=True)
+    torch.cuda.empty_cache()
+    c2 = None
+    if args.config == "c3" and world == 1 and not args.no_c2 and args.n is None:
+        a2 = copy.copy(args)
+        a2.config, a2.nxy, a2.n, a2.nz, a2.m, a2.cfg_name = "c2", 128, 128, 128, 8, "C2 configs[1]"
+        a2.steps, a2.warmup = max(args.steps, 200), max(args.warmup, 10)
+        r2 = measure(a2, world, rank, local, full=False)
+        torch.cuda.empty_cache()
+        c2 = {"value": r2["value"], "unit": "GB/s", "ms_per_step": r2["ms_per_step"], "steps": a2.steps,
+              "label": l2_label(r2["N"]),
+              "workload": f"C2 configs[1]: 3D 128x128x128 7-point Helmholtz manufactured sequence, QR(8) + EXTRAP(3,8)",
+              "dofs": r2["N"], "roofline": r2["roofline"], "kernels": r2["kernels"], "gpu_launches": r2["launches"],
+              "clocks": r2["clocks"]}
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(args, n, M, p, r["N"])
+    if rank != 0:
+        return
+    N, P, nzg = r["N"], r["P"], r["z"][2]
+    strong = args.scaling == "strong"
+    if strong:
+        workload = (f"{args.cfg_name}: 3D {n}x{n}x{nzg} 7-point manufactured sequence (fixed global grid, "
+                    f"{r['N_total']} DOFs) split over {world} GPU(s) in z-slabs, QR({M}) + EXTRAP({p},{M})")
+    else:
+        workload = (f"{args.cfg_name}: 3D {n}x{n}x{args.nz} 7-point manufactured sequence per GPU, "
+                    f"QR({M}) + EXTRAP({p},{M})")
+    l2 = l2_label(N)
+    cfg = {"workload": workload, "dofs_per_gpu": N, "global_dofs": r["N_total"], "input_pool_steps": P,
+           "timing": ("K per-step event windows summed; inputs regenerated between steps outside the windows "
+                      "(history + inputs exceed HBM)") if r["regen"] else "one event window over K steps",
+           "history_m": M, "degree": p, "prefill_steps": r["prefill"], "bytes_per_step_per_gpu": r["step_bytes"],
+           "bytes_model": "QR (8M+4)*8N + EXTRAP (nnz(beta)+1)*8N + push copy 2*8N", "extrap_nnz": r["nnz"],
+           "l2": l2 if l2 else (("fresh inputs every step" if P == args.steps + args.warmup + r["prefill"]
+                                 else f"inputs cycled over {P} steps (1 step re-enters after {P - 1} others)")
+                                + f"; every vector {8 * N / 1e9:.2f} GB > L2 126 MB: HBM measurement"),
+           "parallelism": f"dof-shard{world}" if world > 1 else "single",
+           "exchange": (args.exchange if world > 1 else "none"),
+           "mode": "TEST: all ranks on one GPU" if args.same_gpu else "one rank per GPU"}
+    if strong:
+        cfg["slab_planes"] = [list(partition(args, world, q)[1:]) for q in range(world)]
+    out = {"metric": METRIC, "value": r["value"], "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+           "warmup": args.warmup, "ms_per_step": r["ms_per_step"], "higher_is_better": True,
+           "scaling": args.scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": cfg,
+           "gpu_launches": r["launches"], "roofline": r["roofline"], "kernels": r["kernels"],
+           "step_stats": r["step_stats"], "fill_phase": r["fill_phase"], "clocks": r["clocks"], "e2e": r["e2e"],
+           "cpu_baseline": cpu, "c2_l2_assisted": c2, "proj_state": r["proj_state"],
+           "host_enqueue_us_per_step": r["host_us"]}
+    if strong:
+        out["strong_scaling"] = {"t_ms_per_step": r["ms_per_step"], "t1_ms_per_step": args.t1_ms,
+                                 "efficiency": (args.t1_ms / (world * r["ms_per_step"])) if args.t1_ms else None,
+                                 "definition": "E(N) = t(1) / (N t(N)) at a fixed global grid (SURVEY §8(d))"}
+    print(json.dumps(out), flush=True)
+
+
+def run_dry(args, world, rank):
+    """--dry-run: the partition plan only (no GPU): every rank's z-planes, gathered to rank 0."""
+    import torch.distributed as dist
+
+    nzg, z0, z1 = partition(args, world, rank)
+    mine = [rank, z0, z1, args.nxy * args.nxy * (z1 - z0)]
+    allp = [None] * world
+    if world > 1:
+        dist.all_gather_object(allp, mine)
+    else:
+        allp = [mine]
     if rank == 0:
-        out = {"metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": K, "warmup": W,
-               "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-               "dtype": "f64", "data": "synthetic",
-               "config": {"workload": f"{args.cfg_name}: 3D {n}x{n}x{nz} 7-point Helmholtz manufactured sequence "
-                                      f"per GPU, QR({M}) + EXTRAP({p},{M})",
-                          "dofs_per_gpu": N, "input_pool_steps": P,
-                          "timing": ("K per-step event windows summed; inputs regenerated between steps outside "
-                                     "the windows (history + inputs exceed HBM)") if regen else "one event window over K steps", "history_m": M, "degree": p, "prefill_steps": prefill,
-                          "bytes_per_step_per_gpu": step_bytes,
-                          "bytes_model": "QR (8M+4)*8N + EXTRAP (nnz(beta)+1)*8N + push copy 2*8N",
-                          "extrap_nnz": nnz,
-                          "l2": (f"fresh inputs every step" if P == S else f"inputs cycled over {P} steps")
-                                + f"; per-step working set {(2 * M + M + 5) * 8 * N / 1e9:.2f} GB > L2 126 MB",
-                          "parallelism": f"dof-shard{world}" if world > 1 else "single",
-                          "exchange": (args.exchange if world > 1 else "none"),
-                          "mode": "TEST: all ranks on one GPU" if args.same_gpu else "one rank per GPU"},
-               "gpu_launches": launches, "roofline": roofline, "kernels": kernels, "step_stats": step_stats,
-               "fill_phase": fill,
-               "clocks": sampler.summary(), "e2e": e2e, "cpu_baseline": cpu,
-               "proj_state": {"d": st["d"], "rho_last": st["rho"]}, "host_enqueue_us_per_step": host_us}
-        print(json.dumps(out), flush=True)
+        print(json.dumps({"dry_run": True, "scaling": args.scaling, "n_gpus": world, "config": args.config,
+                          "nz_global": nzg, "grid": [args.nxy, args.nxy, nzg],
+                          "global_dofs": args.nxy * args.nxy * nzg,
+                          "slabs": [{"rank": q, "z0": a, "z1": b, "dofs": d} for q, a, b, d in allp]}), flush=True)
 
 
 def main():
@@ -574,7 +696,10 @@ def main():
         run_reference(args, world, rank)
         return
     world, rank, local = dist_setup(args)
-    run_ours(args, world, rank, local)
+    if args.dry_run:
+        run_dry(args, world, rank)
+    else:
+        run_ours(args, world, rank, local)
     if world > 1:
         import torch.distributed as dist
 

@@ -88,22 +88,40 @@ const char *ig_last_error(void);
 int ig_set_stream(ig_t h, void *cuda_stream);
 
 /* Projection admission tolerance (AMB-3 reading of PAPER.md:209-215, 246, 302): the new pair is
- * admitted iff ||b~|| > eps_rel * ||A x|| after the two Gram-Schmidt passes.  Default 1e-10. */
+ * admitted iff ||b~|| > eps_rel * ||A x|| after the two Gram-Schmidt passes.  Default 1e-10
+ * (relative).  This deliberately differs from SPEC.md's solver-tied absolute default
+ * 10*eps_solver*max(||b~||, 1) (about 1e-7 relative for eps_solver = 1e-8): the paper only says
+ * the value "will depend on ... the stopping criterion", and with a CG
+ * tolerance of 1e-8 the measured ||b~||/||A x|| floor is 2e-9..5e-8, so the SPEC default rejects
+ * most pairs and tripled QR(8)'s CG iterations.  Callers that want the
+ * solver-tied rule pass eps_rel = 10 * eps_solver here. */
 int ig_set_admit_tol(ig_t h, double eps_rel);
 
 /* Projection kernel schedule.  fused = 1 (default): on a single rank (or with the in-kernel peer
  * exchange, ig_attach_peers) each ig_form_guess / ig_update is ONE persistent kernel whose passes
- * are separated by software grid barriers.  Its grid (SMs x occupancy, or ig_set_grid_limit) must
- * be resident at once: by default it is launched as an ordinary kernel (faster, PDL-chained),
- * which assumes no kernel on another stream holds SMs until this one finishes.  The library
- * orders its own persistent launches across streams of one device (a launch from a different
- * stream than the previous one waits for that stream's work; handles with a grid limit are
- * exempt); env IG_LAUNCH=coop,pdl makes the driver guarantee co-residency against foreign
- * kernels too (cooperative launch).  A barrier
- * that cannot complete gives up after the watchdog time (ig_set_watchdog) and reports
- * IG_E_STATE.  fused = 0, or a handle with an NCCL communicator (ig_attach_comm): one kernel per
- * pass with the NCCL exchange of partial sums between them.  Same arithmetic. */
+ * are separated by software grid barriers, so its grid (SMs x occupancy, or ig_set_grid_limit)
+ * must be resident at once -- see ig_set_launch.  A barrier that cannot complete gives up after
+ * the watchdog time (ig_set_watchdog) and reports IG_E_STATE.  fused = 0, or a handle with an NCCL communicator (ig_attach_comm): one kernel per
+ * pass with the NCCL exchange of partial sums between them.  Same arithmetic.  A handle with
+ * peers attached (ig_attach_peers) always runs the fused kernels (only they read the exchange
+ * windows): ig_set_schedule(h, 0) then returns IG_E_STATE and changes nothing. */
 int ig_set_schedule(ig_t h, int fused);
+
+/* Launch mode of the persistent projection kernels.
+ *   cooperative = 1 (DEFAULT): cooperative launch (PDL-chained as well).  The driver starts the
+ *     grid only when all of its CTAs can be resident, so kernels of OTHER streams that hold SMs
+ *     (the solver, a halo exchange, NCCL) delay the launch instead of stalling a grid barrier:
+ *     safe next to any concurrent work.
+ *   cooperative = 0: ordinary launch.  Correct only while no kernel on another stream holds SMs
+ *     until this one finishes (e.g. the GPU is dedicated to this stream); otherwise the barrier
+ *     waits for the missing CTAs, up to the watchdog time.  The library orders its own plain
+ *     persistent launches across streams of one device (a launch from a different stream than
+ *     the previous one first waits for that stream's work).
+ *   cooperative = -1: the process default (env IG_LAUNCH: "plain" / "coop", plus "pdl"/"nopdl").
+ * Handles with a grid limit (ig_set_grid_limit: virtual ranks sharing one GPU, whose grids are
+ * sized to run side by side) default to the ordinary launch.  Results are bitwise identical in
+ * every mode (same grid, same reduction order). */
+int ig_set_launch(ig_t h, int cooperative);
 
 /* ---------------------------------------------------------------- the hot path */
 
@@ -164,7 +182,11 @@ double *ig_next_slot(ig_t h);
  * projection; the solution window, its order and fill for extrapolation) for restarting a long
  * run.  ig_save_state / ig_load_state sync the handle's stream; the image is only valid for a
  * handle created with the same (N, method, m, degree) on any device.  Multi-rank handles save
- * their local shard; all ranks must load images saved at the same step. */
+ * their local shard; all ranks must load images saved at the same step.  Loading restores the
+ * history, d / ring position and the admission tolerance saved with it; the handle's own launch
+ * and peer-exchange epochs are kept (they only move forward).  A header that does not match the
+ * handle, or ring/dimension fields out of range, give IG_E_ARG and leave the handle unchanged.
+ * (Checkpoint/resume is an auxiliary subsystem, outside the hot-path scope of SURVEY.md §8.) */
 size_t ig_state_bytes(ig_t h);
 int ig_save_state(ig_t h, void *host_buf, size_t bytes);
 int ig_load_state(ig_t h, const void *host_buf, size_t bytes);

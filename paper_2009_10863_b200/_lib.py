@@ -67,6 +67,7 @@ _SIGS = {
     "ig_xwin_ptr": (_P, [_P]),
     "ig_attach_peers": (C.c_int, [_P, C.c_int, C.c_int, _P, C.POINTER(_P)]),
     "ig_set_grid_limit": (C.c_int, [_P, C.c_int]),
+    "ig_set_launch": (C.c_int, [_P, C.c_int]),
     "ig_set_watchdog": (C.c_int, [_P, C.c_double]),
     "ig_profile_read": (C.c_int, [_P, C.c_int, _D, C.POINTER(C.c_int64)]),
 }

@@ -21,7 +21,10 @@ LIB = os.path.join(PKG, "libig.so")
 SOURCES = ["kern_proj.cu", "kern_fused.cu", "kern_extrap.cu", "coeffs.cpp", "api.cpp"]
 HEADERS = [os.path.join(CSRC, "ig_internal.h"), os.path.join(CSRC, "proj_common.cuh"), os.path.join(INCLUDE, "ig.h")]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-FLAGS = [*(["-DIG_U2_MC8=" + os.environ["IG_U2_MC8"]] if os.environ.get("IG_U2_MC8") else []), *(["-DIG_UP1_MC8=" + os.environ["IG_UP1_MC8"]] if os.environ.get("IG_UP1_MC8") else []), *(["-DIG_UU1_MC8=" + os.environ["IG_UU1_MC8"]] if os.environ.get("IG_UU1_MC8") else []), *(["-DIG_FP_MC8=" + os.environ["IG_FP_MC8"]] if os.environ.get("IG_FP_MC8") else []), *(["-DIG_EXU8=" + os.environ["IG_EXU8"]] if os.environ.get("IG_EXU8") else []), *(["-DIG_UX_MC8=" + os.environ["IG_UX_MC8"]] if os.environ.get("IG_UX_MC8") else []), *(["-DIG_TRACE=1"] if os.environ.get("IG_TRACE") else []), "-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xptxas", "-v", f"-I{INCLUDE}", f"-I{CSRC}"]
+FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xptxas", "-v", f"-I{INCLUDE}", f"-I{CSRC}"]
+# Debug build (`python -m paper_2009_10863_b200.build --trace`): per-CTA %globaltimer stamps in the
+# fused update (scripts/trace_phases.py).  The default build has no variants.
+TRACE_FLAGS = ["-DIG_TRACE=1"]
 
 
 def _nvcc() -> str:
@@ -38,12 +41,13 @@ def _stale(target: str, deps) -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(verbose: bool = False, force: bool = False) -> str:
+def build(verbose: bool = False, force: bool = False, trace: bool = False) -> str:
     os.makedirs(BUILD, exist_ok=True)
     nvcc = _nvcc()
+    flags = FLAGS + (TRACE_FLAGS if trace else [])
     # objects built with other flags (e.g. an IG_TRACE=1 debug build) are never reused
     stamp = os.path.join(BUILD, "flags.txt")
-    want = " ".join(ARCH + FLAGS)
+    want = " ".join(ARCH + flags)
     have = open(stamp).read() if os.path.exists(stamp) else None
     if have != want:
         force = True
@@ -54,7 +58,7 @@ def build(verbose: bool = False, force: bool = False) -> str:
         objs.append(o)
         if force or _stale(o, [s] + HEADERS):
             lang = [] if src.endswith(".cu") else ["-x", "cu"] if False else []
-            jobs.append((s, o, [nvcc, *ARCH, *FLAGS, *lang, "-c", s, "-o", o]))
+            jobs.append((s, o, [nvcc, *ARCH, *flags, *lang, "-c", s, "-o", o]))
 
     def run(job):
         s, o, cmd = job
@@ -83,4 +87,4 @@ def build(verbose: bool = False, force: bool = False) -> str:
 
 
 if __name__ == "__main__":
-    build(verbose=True, force="--force" in sys.argv)
+    build(verbose=True, force="--force" in sys.argv, trace="--trace" in sys.argv)

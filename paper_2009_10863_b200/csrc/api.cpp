@@ -50,8 +50,9 @@ ig::LaunchFlags ig::launch_flags() {
         const char *e = getenv("IG_LAUNCH");
         if (e) {
             std::string v(e);
-            r.coop = v.find("coop") != std::string::npos;
-            r.pdl = v.find("pdl") != std::string::npos;
+            if (v.find("coop") != std::string::npos) r.coop = true;
+            if (v.find("plain") != std::string::npos || v == "none" || v == "pdl") r.coop = false;
+            r.pdl = v.find("pdl") != std::string::npos && v.find("nopdl") == std::string::npos;
         }
         return r;
     }();
@@ -170,6 +171,7 @@ struct ig_ctx {
     bool fused = true;  // persistent fused kernels when G == 1 (ig_set_schedule)
     ig_comm_ctx *comm = nullptr;
     int max_grid = 0;   // ig_set_grid_limit
+    int coop = -1;      // ig_set_launch: 1 cooperative, 0 plain, -1 process default (IG_LAUNCH)
     unsigned long long watchdog_ns = WATCHDOG_NS;  // ig_set_watchdog
     // in-kernel peer exchange (ig_attach_peers)
     XWin *xwin = nullptr;
@@ -281,15 +283,20 @@ ProjArgs proj_args(ig_t h) {
     a.max_grid = h->max_grid;
     a.watchdog_ns = h->watchdog_ns;
     a.xc = h->xc;
+    // default: cooperative, except grid-limited handles (ranks sharing one GPU, ig_set_grid_limit),
+    // whose grids are sized to be co-resident with their peers' grids and must run concurrently
+    a.coop = h->coop >= 0 ? h->coop : ((launch_flags().coop && h->max_grid == 0) ? 1 : 0);
     return a;
 }
 
 // Fused persistent kernels are used on one rank and with the in-kernel peer exchange; a NCCL
 // communicator without peer windows uses one kernel per pass with NCCL between them.
-bool use_fused(ig_t h) { return h->fused && (h->G == 1 || h->xc.G > 1); }
+// Peers attached (ig_attach_peers) always use the fused kernels: only they read the exchange
+// windows (the split kernels would sum this rank's partials alone).
+bool use_fused(ig_t h) { return h->xc.G > 1 || (h->fused && h->G == 1); }
 
-// Full-grid persistent kernels of DIFFERENT streams on one device must not overlap: each needs its
-// whole grid resident at once (non-cooperative launch, see ig_set_schedule), and two grids whose
+// Plain-launched (ig_set_launch(h, 0)) full-grid persistent kernels of DIFFERENT streams on one
+// device must not overlap: each needs its whole grid resident at once, and two grids whose
 // CTAs interleave could each wait at a barrier for CTAs the other one holds.  Handles sharing a
 // stream are ordered by the stream (the common case: nothing to do); a persistent launch from a
 // different stream than the previous one on this device first waits for everything enqueued on
@@ -308,6 +315,7 @@ PersistOrder &persist_order(int dev) {
 }
 template <class F> int persistent_launch(ig_t h, F &&launch) {
     if (h->max_grid > 0) return launch();
+    if (proj_args(h).coop) return launch();  // cooperative: the driver guarantees co-residency
     cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
     if (cudaStreamIsCapturing(h->stream, &cap) != cudaSuccess) cudaGetLastError();
     if (cap != cudaStreamCaptureStatusNone) return launch();  // graph capture: replays order themselves
@@ -492,6 +500,8 @@ int ig_set_stream(ig_t h, void *s) {
 
 int ig_set_schedule(ig_t h, int fused) {
     if (!h) return set_err(IG_E_ARG, "NULL handle");
+    if (!fused && h->xc.G > 1)
+        return set_err(IG_E_STATE, "peers are attached: the in-kernel exchange needs the fused schedule");
     h->fused = fused != 0;
     return IG_OK;
 }
@@ -564,13 +574,26 @@ int ig_load_state(ig_t h, const void *host_buf, size_t bytes) {
         return set_err(IG_E_ARG, "state image is for (method %d, N %lld, m %d, degree %d)", hd.method,
                        (long long)hd.N, hd.M, hd.degree);
     if (bytes < ig_state_bytes(h)) return set_err(IG_E_ARG, "state image truncated");
+    if (hd.nslab != nslabs(h) || hd.head < 0 || hd.head >= h->M || hd.fill < 0 || hd.fill > h->M ||
+        !(hd.eps >= 0.0))
+        return set_err(IG_E_ARG, "corrupt state image (nslab %d, head %d, fill %d)", hd.nslab, hd.head, hd.fill);
     p += sizeof hd;
     if (is_proj(h->method)) {
         Ctrl c;
         memcpy(&c, p, sizeof c);
+        if (c.d < 0 || c.d > h->M || c.deff < 0 || c.deff > h->M)
+            return set_err(IG_E_ARG, "corrupt state image (d %d)", c.d);
         for (unsigned &t : c.ticket) t = 0;  // transient launch state is never part of a checkpoint
         c.bar[0] = c.bar[1] = c.dyn3[0] = c.dyn3[1] = 0;
         c.err = 0;
+        // the live handle's launch epoch and peer-exchange epochs stay: every rank's window flags
+        // only move forward (an older image's epochs would let the next exchange pass on stale
+        // flags), and the barrier counters zeroed above belong to the live epoch's parities
+        Ctrl live;
+        CUDA_OK(cudaMemcpyAsync(&live, h->ctrl, sizeof live, cudaMemcpyDeviceToHost, h->stream));
+        CUDA_OK(cudaStreamSynchronize(h->stream));
+        c.epoch = live.epoch;
+        memcpy(c.xepoch, live.xepoch, sizeof c.xepoch);
         CUDA_OK(cudaMemcpyAsync(h->ctrl, &c, sizeof c, cudaMemcpyHostToDevice, h->stream));
         CUDA_OK(cudaStreamSynchronize(h->stream));  // c is a stack object
         p += sizeof(Ctrl);
@@ -994,6 +1017,12 @@ int ig_attach_comm(ig_t h, ig_comm_t c) {
     CUDA_OK(cudaMemset(gb, 0, sizeof(double) * PS * NSTAGE * c->nranks));
     h->gath = gb;
     h->G = c->nranks;
+    return IG_OK;
+}
+
+int ig_set_launch(ig_t h, int cooperative) {
+    if (!h || cooperative < -1 || cooperative > 1) return set_err(IG_E_ARG, "bad handle or launch mode");
+    h->coop = cooperative;
     return IG_OK;
 }
 

@@ -80,6 +80,7 @@ struct ProjArgs {
     int max_grid;          // cap on the persistent kernels' grid (0: SMs x occupancy)
     unsigned long long watchdog_ns;  // spin-wait limit of grid barriers / peer exchange
     Exchange xc;           // in-kernel peer exchange (xc.G > 1) for the fused kernels
+    int coop;              // persistent kernels: 1 cooperative launch, 0 plain launch (host side only)
 };
 
 struct ExtrapArgs {
@@ -98,16 +99,19 @@ struct ExtrapBatch {
 };
 
 // ----------------------------------------------------------------------------- launch policy
-// Process-wide launch flags (env IG_LAUNCH, comma list of "coop", "pdl"; default "pdl"):
-//   coop: persistent fused kernels use cooperative launch (co-residency guaranteed by the driver).
-//         Without it (default) they rely on grid = SMs x occupancy being resident at once, which
-//         holds whenever no other stream pins SMs indefinitely; measured 1.7% faster at C2.
+// Process-wide launch defaults (env IG_LAUNCH, comma list of "coop", "plain", "pdl", "nopdl";
+// default coop + pdl; a handle overrides the coop choice with ig_set_launch):
+//   coop: persistent fused kernels use cooperative launch: the driver only starts the grid when
+//         all of its CTAs can be resident, so a kernel of another stream (a halo exchange, NCCL,
+//         the solver) holding SMs delays the launch instead of stalling a grid barrier.
+//   plain: ordinary launch; relies on grid = SMs x occupancy being resident at once, which holds
+//         whenever no other stream pins SMs (ig_set_launch documents the trade).
 //   pdl : programmatic dependent launch: every libig kernel may be launched while its stream
 //         predecessor is finishing; each kernel executes griddepcontrol.wait (waits for the full
 //         completion + memory flush of the predecessor) before touching memory, and triggers its
 //         dependents once its streaming passes are done (C2: 232.2 -> 224.3 us/step).
 struct LaunchFlags {
-    bool coop = false;
+    bool coop = true;
     bool pdl = true;
 };
 LaunchFlags launch_flags();
@@ -126,7 +130,7 @@ static cudaError_t launch_ex(void (*kern)(Exp...), int grid, cudaStream_t s, boo
     cfg.stream = s;
     cudaLaunchAttribute at[2];
     int na = 0;
-    if (coop && f.coop) {
+    if (coop) {
         at[na].id = cudaLaunchAttributeCooperative;
         at[na].val.cooperative = 1;
         ++na;

@@ -108,13 +108,15 @@ template <class K> static int grid_for_x(K kern, int64_t nv, int nsm) {
     return (int)g;
 }
 
-#ifndef IG_EXU8
-#define IG_EXU8 2  // elements per trip of the 8-term extrapolation combine (A/B on C2: 1 -> 207.8, 2 -> 207.4 us/step)
-#endif
+// Elements per trip of the combine (bytes in flight per thread), by term bucket; the 8-term value
+// was A/B-measured on C2 (1 -> 207.8, 2 -> 207.4 us/step).
+template <int FC> struct ExtrapTune {
+    static constexpr int U = FC <= 2 ? 4 : (FC <= 4 ? 2 : (FC == 8 ? 2 : 1));
+};
 template <int FC>
 static void launch_fc(const ExtrapArgs &a, int vec, int nsm, cudaStream_t s) {
     if (vec == 2) {
-        constexpr int U = FC <= 2 ? 4 : (FC <= 4 ? 2 : (FC == 8 ? IG_EXU8 : 1));
+        constexpr int U = ExtrapTune<FC>::U;
         auto k = k_extrap<FC, 2, U>;  // U strided elements per trip when few streams
         launch_ex(k, grid_for_x(k, a.N / 2, nsm), s, false, a);
     } else {

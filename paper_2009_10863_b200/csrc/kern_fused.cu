@@ -39,19 +39,6 @@ extern "C" int ig_debug_trace_read_form(unsigned long long *host, int n) {
 #define TRACE_F(slot) do { } while (0)
 #endif
 
-#ifndef IG_UU1_MC8
-#define IG_UU1_MC8 2  // update pass-1 elements per trip at M = 8 (A/B knob)
-#endif
-#ifndef IG_FP_MC8
-#define IG_FP_MC8 1  // form pass-2 trips prefetched across the barrier at M = 8 (A/B knob, with IG_UX_MC8)
-#endif
-#ifndef IG_UX_MC8
-#define IG_UX_MC8 3  // form pass-2 elements per trip at M = 8 (A/B: 2x2 prefetched 207.4, 3x1 207.2, 4x1 207.8, 1x4 212.2 us)
-#endif
-#ifndef IG_UP1_MC8
-#define IG_UP1_MC8 3  // form pass-1 unroll at M = 8 (A/B: 2 -> 208.1, 3 -> 207.8, 4 -> 208.0 us/step at C2)
-#endif
-
 namespace ig {
 
 // Second block-partial buffer so that a fast CTA's pass-2 partials never overwrite pass-1
@@ -86,7 +73,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_form_fused(ProjArgs a) {
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     const int64_t i_first = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     // ---- pass 1: alpha = B~^T b (UP strided elements per trip: read-only, more bytes in flight)
-    constexpr int UP = (MC == 8) ? IG_UP1_MC8 : U;
+    constexpr int UP = FusedUnroll<MC>::FORM_P1;
     double v[MC + 1];
 #pragma unroll
     for (int k = 0; k <= MC; ++k) v[k] = 0.0;
@@ -114,8 +101,8 @@ __global__ void __launch_bounds__(THREADS, 1) k_form_fused(ProjArgs a) {
     }
     // the first FP trips of pass 2 are in flight across the barrier (the bubble is ~2-4 us: one
     // trip of 1 CTA/SM covers ~1.5 us of the SM's bandwidth share)
-    constexpr int FP = (MC == 8) ? IG_FP_MC8 : ((MC < 8) ? 2 : 1);
-    constexpr int UX = (MC == 8) ? IG_UX_MC8 : U;  // pass-2 elements per trip (A/B knob)
+    constexpr int FP = FusedUnroll<MC>::FORM_PF;
+    constexpr int UX = FusedUnroll<MC>::FORM_P2;
     XTrip<MC, UX, V> pre[FP];
 #pragma unroll
     for (int f = 0; f < FP; ++f) xtrip_load(pre[f], a, i_first + f * UX * stride, stride, nv, d, ps);
@@ -215,7 +202,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_update_fused(ProjArgs a) {
     double v[MC + 1];
 #pragma unroll
     for (int k = 0; k <= MC; ++k) v[k] = 0.0;
-    constexpr int UU1 = (MC == 8) ? IG_UU1_MC8 : U;  // pass-1 elements per trip (A/B knob)
+    constexpr int UU1 = U;  // pass-1 elements per trip
     for (int64_t i0 = i_first; i0 < nv; i0 += UU1 * stride) u1_trip<MC, UU1, V>(a, i0, stride, nv, pend, deff, gc, gs, v, pol.keep);
     if (tail) u1_trip<MC, 1, double>(a, a.N - 1, 1, a.N, pend, deff, gc, gs, v, pol.keep);
     // Serpentine order: pass 2 walks the vectors BACKWARDS, so it starts on the B~/Ax lines pass 1
@@ -277,7 +264,9 @@ __global__ void __launch_bounds__(THREADS, 1) k_update_fused(ProjArgs a) {
         const double nb = sqrt(fmax(nb2, 0.0)), nAx = sqrt(nAx2);
         s_nb = nb;
         s_nAx = nAx;
-        s_adm = (deff > 0) ? (nb > a.eps * nAx) : (nAx > 0.0);  // AMB-3 / AMB-6
+        // AMB-3 / AMB-6; a non-finite sum never admits (the history stays unchanged)
+        const bool fin = isfinite(nAx2) && (deff == 0 || isfinite(nb2));
+        s_adm = fin && ((deff > 0) ? (nb > a.eps * nAx) : (nAx > 0.0));
     }
     __syncthreads();
     const bool adm = s_adm != 0;
@@ -387,28 +376,16 @@ __global__ void __launch_bounds__(THREADS, 1) k_update_fused(ProjArgs a) {
     TRACE(7);
 }
 
-// ------------------------------------------------------------------ launchers (cooperative iff IG_LAUNCH has "coop")
+// ------------------------------------------------------------------ launchers (cooperative unless the handle asks for plain)
 template <class K> static cudaError_t coop_launch(K kern, const ProjArgs &a, int nsm, cudaStream_t s) {
     static_assert(sizeof(ProjArgs) < 4096, "kernel parameters");
     int occ = cached_occupancy((const void *)kern);
     if (occ < 1) return cudaErrorInvalidConfiguration;
     if (occ > 4) occ = 4;
     int grid = nsm * occ;
-    // Optional (IG_MIN_TRIPS): fewer CTAs for small vectors (>= that many grid-stride trips per
-    // thread).  Measured: it only slows small N down (1e5 DOFs, QR(8): 27.7 us at 1 CTA/SM vs
-    // 33.9 us at 4 trips/thread) -- the per-call cost there is latency, not barrier width.
-    static const int min_trips = [] {
-        const char *e = getenv("IG_MIN_TRIPS");
-        return e ? atoi(e) : 0;
-    }();
-    if (min_trips > 0) {
-        const int64_t nv = a.N / 2;
-        const int64_t want = (nv + (int64_t)THREADS * min_trips - 1) / ((int64_t)THREADS * min_trips);
-        if (want < grid) grid = want < 1 ? 1 : (int)want;
-    }
     if (a.max_grid > 0 && grid > a.max_grid) grid = a.max_grid;
     if (grid > MAXB) grid = MAXB;
-    return launch_ex(kern, grid, s, true, a);
+    return launch_ex(kern, grid, s, a.coop != 0, a);
 }
 
 static int mcb(int M) { return M <= 1 ? 1 : M <= 2 ? 2 : M <= 4 ? 4 : M <= 8 ? 8 : M <= 16 ? 16 : 32; }

@@ -236,7 +236,9 @@ __global__ void __launch_bounds__(THREADS, 1) k_u3(ProjArgs a) {
         const double nb = sqrt(fmax(nb2, 0.0)), nAx = sqrt(nAx2);
         s_nb = nb;
         s_nAx = nAx;
-        s_adm = (deff > 0) ? (nb > a.eps * nAx) : (nAx > 0.0);  // AMB-3 / AMB-6
+        // AMB-3 / AMB-6; a non-finite sum never admits (the history stays unchanged)
+        const bool fin = isfinite(nAx2) && (deff == 0 || isfinite(nb2));
+        s_adm = fin && ((deff > 0) ? (nb > a.eps * nAx) : (nAx > 0.0));
     }
     __syncthreads();
     const bool adm = s_adm != 0;

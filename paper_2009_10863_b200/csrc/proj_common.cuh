@@ -387,9 +387,6 @@ __device__ __forceinline__ void u2_trip(const ProjArgs &a, int64_t i0, int64_t s
     }
 }
 
-#ifndef IG_U2_MC8
-#define IG_U2_MC8 2
-#endif
 // Per-column coefficient access: registers for MC <= 8, shared memory (re-read at each use) for
 // larger buckets.  Fills `reg` from `smem` when registers are used and returns the pointer type
 // the trip functions index.
@@ -408,11 +405,21 @@ template <int MC> struct Coef {
     }
 };
 
-// Unroll of the fused kernels' d+1-stream passes (registers are sized by the X~ pass anyway).
+// Per-bucket tuning of the fused kernels (elements per trip = bytes in flight per thread; the
+// M = 8 entries were A/B-measured on the C2 bench):
+//   FORM_P1  form pass 1 (alpha = B~^T b)        M=8: 2 -> 208.1, 3 -> 207.8, 4 -> 208.0 us/step
+//   FORM_P2  form pass 2 (x0 = X~ alpha)         M=8: 2x2 prefetched 207.4, 3x1 207.2, 4x1 207.8
+//   FORM_PF  form pass-2 trips prefetched across the grid barrier
+//   U        update pass 1 (B~ rotation + c1)    M=8: 2 -> 208.5, 3 -> 210.7
+//   U2       update pass 2 (mostly L2 hits)      M=8: 1 -> 214.2, 2 -> 208.5, 3 -> 209.1
+//   U3       update pass 3 (X~ pass, 2d+2 streams)
 template <int MC> struct FusedUnroll {
     static constexpr int U = MC <= 4 ? 4 : (MC <= 8 ? 2 : 1);
-    static constexpr int U3 = MC <= 2 ? 4 : (MC <= 4 ? 2 : 1);  // X~ pass (2d+2 streams)
-    static constexpr int U2 = MC <= 4 ? 4 : (MC <= 8 ? IG_U2_MC8 : 1);  // pass 2 (mostly L2 hits)
+    static constexpr int U3 = MC <= 2 ? 4 : (MC <= 4 ? 2 : 1);
+    static constexpr int U2 = MC <= 4 ? 4 : (MC <= 8 ? 2 : 1);
+    static constexpr int FORM_P1 = MC == 8 ? 3 : U;
+    static constexpr int FORM_P2 = MC == 8 ? 3 : U;
+    static constexpr int FORM_PF = MC == 8 ? 1 : (MC < 8 ? 2 : 1);
     // For MC >= 16 the per-column coefficients (c1, c2, Givens c/s) are read from shared memory
     // at each use instead of living in 4*MC registers, which the column loads need.
     static constexpr bool SMEM_COEF = MC >= 16;

@@ -309,6 +309,11 @@ def ig_set_grid_limit(h, max_blocks: int) -> None:
     _check(lib().ig_set_grid_limit(h, int(max_blocks)), "ig_set_grid_limit")
 
 
+def ig_set_launch(h, cooperative: int) -> None:
+    """Persistent kernels: 1 cooperative (default), 0 plain launch, -1 process default (ig.h)."""
+    _check(lib().ig_set_launch(h, int(cooperative)), "ig_set_launch")
+
+
 def ig_set_watchdog(h, seconds: float) -> None:
     _check(lib().ig_set_watchdog(h, float(seconds)), "ig_set_watchdog")
 

@@ -237,3 +237,183 @@ def test_projection_fields_on_different_streams_are_ordered_and_correct():
     for ig, ora in zip(igs, oras):
         assert ig.stats()["d"] == ora.d  # stats() syncs and reports a watchdog trip as an error
         ig.close()
+
+
+def test_non_finite_first_pair_is_not_admitted():
+    """d = 0 and ||A x||^2 = Inf: the pair must not enter the history (ig.h: NaN/Inf sums leave it
+    unadmitted) -- the next guess leaves the caller's fallback untouched (d == 0)
+    and the event is reported as IG_E_STATE."""
+    from paper_2009_10863_b200 import IGError, InitialGuess
+
+    N = 3000
+    for fused in (True, False):
+        ig = InitialGuess(N, "proj_qr", 4, fused=fused)
+        x = torch.rand(N, dtype=torch.float64, device="cuda")
+        big = x.clone()
+        big[5] = 1e200  # ||A x||^2 overflows to Inf, entries stay finite
+        ig.update(x, big)
+        fb = torch.full((N,), 3.0, dtype=torch.float64, device="cuda")
+        ig.form_guess(torch.rand(N, dtype=torch.float64, device="cuda"), fb)
+        assert torch.equal(fb.cpu(), torch.full((N,), 3.0, dtype=torch.float64)), fused
+        with pytest.raises(IGError, match="non-finite"):
+            ig.stats()
+        ig.close()
+
+
+def test_load_state_rejects_corrupt_headers():
+    """ig_load_state validates the ring / dimension fields before touching the handle."""
+    import struct
+
+    from paper_2009_10863_b200 import IGError, InitialGuess
+
+    g = Grid(20, 2)
+    for method, M, p in (("extrap_ls", 5, 2), ("proj_qr", 5, 0)):
+        a = InitialGuess(g.N, method, M, p)
+        for b, x, Ax in _seq(g, M + 2):
+            a.update(torch.from_numpy(x).cuda(), torch.from_numpy(Ax).cuda())
+        img = bytearray(a.save_state())
+        for off, val in ((20, M), (20, -1), (32, M + 1), (36, 2 * M + 3)):  # head, fill, nslab
+            bad = bytearray(img)
+            struct.pack_into("<i", bad, off, val)
+            with pytest.raises(IGError, match="corrupt"):
+                a.load_state(bytes(bad))
+        a.load_state(bytes(img))  # the intact image still loads
+        a.close()
+
+
+def test_checkpoint_restore_with_peers_attached():
+    """Load an OLDER image into live handles wired as virtual ranks of the in-kernel exchange: the
+    exchange epochs must stay monotonic (ig_load_state keeps the live ones), so the resumed run
+    matches the unsharded oracle restored at the same step, with identical decisions on all ranks."""
+    import copy
+
+    from paper_2009_10863_b200 import InitialGuess, attach_virtual_ranks, ig_set_grid_limit, shard_range
+
+    G, M = 2, 5
+    g = Grid(37, 2)
+    nsm = torch.cuda.get_device_properties(0).multi_processor_count
+    ranges = [shard_range(g.N, G, r) for r in range(G)]
+    streams = [torch.cuda.Stream() for _ in range(G)]
+    igs = [InitialGuess(hi - lo, "proj_qr", M, stream=streams[r]) for r, (lo, hi) in enumerate(ranges)]
+    for ig in igs:
+        ig_set_grid_limit(ig.h, max(1, nsm // G))
+    attach_virtual_ranks([ig.h for ig in igs])
+    ora = ProjQR(g.N, M)
+    seq = _seq(g, 3 * M + 6)
+
+    def step(n, check):
+        b, x, Ax = seq[n]
+        x0s = [torch.zeros(hi - lo, dtype=torch.float64, device="cuda") for lo, hi in ranges]
+        ins = [tuple(torch.from_numpy(v[lo:hi].copy()).cuda() for v in (b, x, Ax)) for lo, hi in ranges]
+        torch.cuda.synchronize()  # inputs resident before the ranks' streams read them
+        for r in range(G):
+            igs[r].form_guess(ins[r][0], x0s[r])
+        for r in range(G):
+            igs[r].update(ins[r][1], ins[r][2])
+        torch.cuda.synchronize()
+        got = torch.cat([t.cpu() for t in x0s]).numpy()
+        ref = ora.form_guess(b, np.zeros(g.N))
+        if check:
+            assert np.linalg.norm(got - ref) <= 1e-11 * max(np.linalg.norm(ref), 1e-300), n
+        ora.update(x, Ax)
+        st = [ig.stats() for ig in igs]
+        assert all(s["d"] == ora.d for s in st) and len({(s["admitted"], s["rho"]) for s in st}) == 1, n
+
+    ck = M + 2
+    for n in range(ck):
+        step(n, True)
+    imgs = [ig.save_state() for ig in igs]
+    ora_ck = copy.deepcopy(ora)
+    for n in range(ck, ck + M + 3):  # move the exchange epochs well past the image's
+        step(n, True)
+    for ig, img in zip(igs, imgs):
+        ig.load_state(img)
+    ora = ora_ck
+    for n in range(ck, len(seq)):
+        step(n, True)
+    for ig in igs:
+        ig.close()
+
+
+def test_peers_force_the_fused_schedule():
+    """A handle asked for the split schedule and then wired to peers runs the fused kernels (the
+    only ones that read the exchange windows); asking for the split schedule afterwards fails."""
+    from paper_2009_10863_b200 import IGError, InitialGuess, attach_virtual_ranks, ig_set_grid_limit, ig_set_schedule
+    from paper_2009_10863_b200 import shard_range
+
+    G, M = 2, 4
+    g = Grid(33, 2)
+    ranges = [shard_range(g.N, G, r) for r in range(G)]
+    streams = [torch.cuda.Stream() for _ in range(G)]
+    igs = [InitialGuess(hi - lo, "proj_qr", M, stream=streams[r], fused=False) for r, (lo, hi) in enumerate(ranges)]
+    for ig in igs:
+        ig_set_grid_limit(ig.h, 16)
+    attach_virtual_ranks([ig.h for ig in igs])
+    with pytest.raises(IGError, match="fused schedule"):
+        ig_set_schedule(igs[0].h, False)
+    ora = ProjQR(g.N, M)
+    for n, (b, x, Ax) in enumerate(_seq(g, 2 * M + 3)):
+        x0s = [torch.zeros(hi - lo, dtype=torch.float64, device="cuda") for lo, hi in ranges]
+        ins = [tuple(torch.from_numpy(v[lo:hi].copy()).cuda() for v in (b, x, Ax)) for lo, hi in ranges]
+        torch.cuda.synchronize()  # inputs resident before the ranks' streams read them
+        for r in range(G):
+            igs[r].form_guess(ins[r][0], x0s[r])
+        for r in range(G):
+            igs[r].update(ins[r][1], ins[r][2])
+        torch.cuda.synchronize()
+        got = torch.cat([t.cpu() for t in x0s]).numpy()
+        ref = ora.form_guess(b, np.zeros(g.N))
+        assert np.linalg.norm(got - ref) <= 1e-11 * max(np.linalg.norm(ref), 1e-300), n
+        ora.update(x, Ax)
+    for ig in igs:
+        ig.close()
+
+
+@pytest.mark.timeout(300)
+@pytest.mark.parametrize("mode", ["default", "plain"])
+def test_persistent_update_next_to_a_foreign_kernel(mode):
+    """A foreign kernel on another stream holds most SMs (227 KB of shared memory per CTA, so no
+    libig CTA fits beside it) for 1.5 s while ig_update is enqueued -- the situation of a solver,
+    halo-exchange or NCCL kernel running concurrently with the guess machinery.
+    Default (cooperative) launch: the driver starts the persistent grid only when all of its CTAs
+    fit, so no grid barrier waits on CTAs that cannot run: no watchdog trip (0.5 s), oracle
+    parity.  Plain launch: the resident CTAs wait at the first barrier for the rest -- the hazard
+    the default removes (the 0.5 s watchdog must fire)."""
+    from paper_2009_10863_b200 import IGError, InitialGuess, ig_set_launch, ig_set_watchdog
+    from support import hog_lib  # tests/support (tests/ is on sys.path under pytest)
+
+    hog = hog_lib()
+    nsm = torch.cuda.get_device_properties(0).multi_processor_count
+    g = Grid(256, 2)  # N = 65536
+    seq = _seq(g, 6)
+    ora = ProjQR(g.N, 4)
+    ig = InitialGuess(g.N, "proj_qr", 4)
+    if mode == "plain":
+        ig_set_launch(ig.h, 0)
+    ig_set_watchdog(ig.h, 0.5)
+    for b, x, Ax in seq[:4]:  # history filled, kernels warm
+        ig.update(torch.from_numpy(x).cuda(), torch.from_numpy(Ax).cuda())
+        ora.update(x, Ax)
+    torch.cuda.synchronize()
+    started = torch.zeros(1, dtype=torch.int64, device="cuda")
+    foreign = torch.cuda.Stream()
+    nblk = nsm - 16
+    rc = hog.hog_launch(nblk, 227 * 1024, int(1.5e9), started.data_ptr(), foreign.cuda_stream)
+    assert rc == 0, rc
+    while int(started.item()) < nblk:  # every foreign CTA holds its SM (item() syncs the default stream only)
+        pass
+    b, x, Ax = seq[4]
+    x0 = torch.zeros(g.N, dtype=torch.float64, device="cuda")
+    ig.form_guess(torch.from_numpy(b).cuda(), x0)
+    ig.update(torch.from_numpy(x).cuda(), torch.from_numpy(Ax).cuda())
+    if mode == "plain":
+        with pytest.raises(IGError, match="watchdog"):
+            ig.stats()
+    else:
+        st = ig.stats()
+        ref = ora.form_guess(b, np.zeros(g.N))
+        assert np.linalg.norm(x0.cpu().numpy() - ref) <= 1e-11 * np.linalg.norm(ref)
+        ora.update(x, Ax)
+        assert st["d"] == ora.d
+    torch.cuda.synchronize()
+    ig.close()

@@ -1,11 +1,25 @@
-"""Closed loop (BASELINE north_star): each side runs the harness CG from its own guesses and feeds
-its own solutions back into its own history, on the configs[0] sequence (2D 32x32 Helmholtz,
-prescribed smooth RHS, 40 steps, INITRESID eps = 1e-8, fallback LAST); per-step CG iteration
-counts of the CUDA path and the oracle must agree within +-1.  Both sides run the SAME harness CG
-arithmetic (torch fp64 on the host): the CUDA library's guesses are copied out and its solutions
-copied back, so the comparison isolates the initial-guess implementations (a device CG would add
-its own reduction-order rounding to the closed loop and make the counts drift apart).  Also checks the qualitative ordering the paper reports (§6.3):
-projection needs fewer iterations than extrapolation, which needs fewer than LAST."""
+"""Closed loop (BASELINE north_star "downstream CG iteration counts must agree within +-1"; SURVEY
+§8(c) closed-loop protocol) on the configs[0] sequence (2D 32x32 Helmholtz, prescribed smooth RHS,
+40 steps, Jacobi-PCG INITRESID eps = 1e-8, fallback LAST), for all five
+methods (QR, EXTRAP, CLASSIC, SPEXTRAP).  Both sides run the SAME harness CG arithmetic (torch
+fp64 on the host): the CUDA library's guesses are copied out and its solutions copied back, so the
+comparison isolates the initial-guess implementations.  Three protocols:
+
+* identical systems, oracle-driven: the oracle's closed loop feeds both histories; per step the CG
+  from each side's guess must take the same count +-1;
+* identical systems, CUDA-driven ("shadowed"): the CUDA path's OWN closed loop (its guesses feed
+  its CG, its solutions feed its history) with the oracle fed the same pairs: every step's guess
+  within 1e-11 of the oracle's and the counts within +-1;
+* fully independent closed loops: per-step counts within +-1 and the same steady-state mean.
+
+The fully closed loop is chaotic at the CG stopping test (DESIGN.md AMB-21): the ORACLE against
+itself, with its guesses perturbed at the 1e-15 rounding level, drifts by up to 3 (QR(8)) / 2
+(EXTRAP(3,8)) iterations per step (tests/golden/closed_loop_envelope.json, written by
+scripts/closed_loop_envelope.py from oracle/ only).  The +-1 of the independent loops therefore
+holds for this implementation pair, not for every correct one; the shadowed protocol is the
+per-step check that stays well posed.  Also checks the qualitative ordering the paper reports
+(§6.3): projection needs fewer iterations than extrapolation, which needs
+fewer than LAST."""
 
 import numpy as np
 import pytest
@@ -92,14 +106,43 @@ def test_downstream_iterations_within_one(method, M, p):
     assert max(abs(d) for d in diffs) <= 1, diffs
 
 
-# Fully closed loops (each side feeds back its own solutions): CG stops at the 1e-8 tolerance, so
-# the two loops legitimately drift apart at that level; the statistics must still agree.
-@pytest.mark.parametrize("method,M,p", METHODS[:3])
-def test_closed_loop_statistics(method, M, p):
+# GPU-driven identical systems ("shadowed" closed loop): the CUDA path runs its own closed loop; the
+# oracle receives the same (x_n, A x_n) pairs, so every step is an open-loop parity point.
+@pytest.mark.parametrize("method,M,p", METHODS)
+def test_shadowed_closed_loop(method, M, p):
+    g = Grid(32, 2)
+    mk_o, mk_g = _makers(g, method, M, p)
+    ora, lib = mk_o(), mk_g()
+    x_prev = torch.zeros(g.N, dtype=torch.float64)
+    diffs, rels = [], []
+    for n in range(40):
+        b = prescribed_rhs(g, n, 1e-3)
+        x0g = x_prev.clone().cuda()
+        lib.form_guess(b.cuda(), x0g)
+        x0g = x0g.cpu()
+        x0o = torch.from_numpy(ora.form_guess(b.numpy(), x_prev.numpy()))
+        rels.append(float(torch.linalg.vector_norm(x0g - x0o)) / max(float(torch.linalg.vector_norm(x0o)), 1e-300))
+        x, it_g, _, _ = pcg(g, b, x0g)  # the CUDA path's guess drives the loop
+        _, it_o, _, _ = pcg(g, b, x0o)
+        diffs.append(it_g - it_o)
+        Ax = helmholtz_apply(g, x)
+        lib.update(x.cuda(), Ax.cuda())
+        ora.update(x.numpy(), Ax.numpy())
+        x_prev = x
+    lib.close()
+    assert max(rels) <= 1e-11, max(rels)
+    assert max(abs(d) for d in diffs) <= 1, diffs
+
+
+# Fully independent closed loops (each side feeds back its own solutions): north_star's +-1 per
+# step, and the same steady-state mean.  See the module docstring / AMB-21 for why this is a
+# property of the implementation pair (the oracle's own rounding-level envelope is wider).
+@pytest.mark.parametrize("method,M,p", METHODS)
+def test_closed_loop_iterations_within_one(method, M, p):
     g = Grid(32, 2)
     mk_o, mk_g = _makers(g, method, M, p)
     it_g, it_o = _run(g, 40, mk_o, mk_g)
-    assert np.max(np.abs(it_g - it_o)) <= 3, (it_g.tolist(), it_o.tolist())
+    assert np.max(np.abs(it_g - it_o)) <= 1, (it_g.tolist(), it_o.tolist())
     assert abs(it_g[10:].mean() - it_o[10:].mean()) <= 0.5
 
 

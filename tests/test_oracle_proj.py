@@ -275,3 +275,35 @@ def test_projection_vs_extrapolation_harness_sequence():
         p.update(x, Ax)
         e.update(x, Ax)
     assert max(resP) < min(resE)
+
+
+def test_closed_loop_envelope_fixture_matches_the_oracle():
+    """tests/golden/closed_loop_envelope.json (scripts/closed_loop_envelope.py, oracle only; DESIGN.md
+    AMB-21) was written by the current oracle: its unperturbed closed-loop CG counts reproduce
+    exactly, and it records the oracle's own rounding-level spread (> 1 for QR(8): the fully
+    closed loop's +-1 is not implied by correctness alone)."""
+    import json
+    import os
+
+    import torch
+
+    from oracle import ExtrapLS, ExtrapSparse, ProjClassic, ProjQR
+    from workloads import Grid, helmholtz_apply, prescribed_rhs
+    from workloads.cg import pcg
+
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "closed_loop_envelope.json")
+    fx = json.load(open(path))
+    g = Grid(32, 2)
+    for key, mk in (("proj_qr(8,0)", lambda: ProjQR(g.N, 8)), ("extrap_ls(8,3)", lambda: ExtrapLS(g.N, 8, 3)),
+                    ("proj_classic(4,0)", lambda: ProjClassic(g.N, 4)),
+                    ("extrap_sparse(8,3)", lambda: ExtrapSparse(g.N, 8, 3))):
+        obj, x_prev, its = mk(), np.zeros(g.N), []
+        for n in range(40):
+            b = prescribed_rhs(g, n, 1e-3)
+            x0 = np.asarray(obj.form_guess(b.numpy(), x_prev.copy()), dtype=np.float64)
+            x, it, _, _ = pcg(g, b, torch.from_numpy(x0))
+            its.append(int(it))
+            obj.update(x.numpy(), helmholtz_apply(g, x).numpy())
+            x_prev = x.numpy()
+        assert its == fx["methods"][key]["unperturbed"], key
+    assert fx["methods"]["proj_qr(8,0)"]["1e-15"]["max_abs_diff"] > 1

@@ -162,16 +162,26 @@ def prescribed_rhs(g: Grid, n: int, dt: float = 1e-3, device="cpu") -> torch.Ten
 
 def manufactured_step_slab(n_xy: int, nz_local: int, rank: int, world: int, n: int, dt: float = 1e-3,
                            eta_rel: float = 1e-8, sigma: float = 1.0, device="cpu", seed: int = SEED):
-    """Rank `rank`'s z-slab of a global n_xy x n_xy x (nz_local*world) manufactured step.
+    """Rank `rank`'s z-slab of a global n_xy x n_xy x (nz_local*world) manufactured step (weak
+    scaling: every rank holds nz_local planes)."""
+    return manufactured_step_zrange(n_xy, nz_local * world, rank * nz_local, (rank + 1) * nz_local, n, dt,
+                                    eta_rel, sigma, device, seed)
+
+
+def manufactured_step_zrange(n_xy: int, nz_global: int, z0: int, z1: int, n: int, dt: float = 1e-3,
+                             eta_rel: float = 1e-8, sigma: float = 1.0, device="cpu", seed: int = SEED):
+    """z-planes [z0, z1) of a global n_xy x n_xy x nz_global manufactured step (strong scaling: a
+    fixed global grid split into contiguous plane ranges of any sizes).
 
     The field and noise are those of the global grid restricted to the slab (contiguous DOF
     range); the harness operator is the 7-point Helmholtz stencil of the slab with
     homogeneous Dirichlet faces (block-diagonal across ranks: a valid SPD operator, no halo
     exchange needed for synthetic timing inputs).
     """
-    nzg = nz_local * world
+    nzg = nz_global
+    nz_local = z1 - z0
     count = n_xy * n_xy * nz_local
-    offset = rank * count
+    offset = z0 * n_xy * n_xy
     idx = torch.arange(offset, offset + count, dtype=torch.int64, device=device)
     xs = [((idx // (n_xy * n_xy)) + 1).to(torch.float64) / (nzg + 1),
           (((idx // n_xy) % n_xy) + 1).to(torch.float64) / (n_xy + 1),
