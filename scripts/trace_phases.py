@@ -1,5 +1,5 @@
 """Per-phase timing of k_update_fused and k_form_fused from a -DIG_TRACE=1 build (globaltimer
-stamps per CTA, SM id per CTA).  IG_TRACE=1 python -m paper_2009_10863_b200.build, then run this."""
+stamps per CTA, SM id per CTA).  python -m paper_2009_10863_b200.build --trace, then run this."""
 import ctypes as C, os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch
