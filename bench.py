@@ -78,6 +78,7 @@ def parse():
     a = p.parse_args()
     # (nx, ny, nz per GPU, M): the z extent is per rank (contiguous z-slabs, weak scaling)
     shape = {"c2": (128, 128, 128, 8), "c3": (512, 512, 512, 8), "c4": (512, 512, 1024, 16)}[a.config]
+    a.n_override = a.n is not None
     if a.n is not None:
         shape = (a.n, a.n, a.n, shape[3])
     a.nxy, a.nz = shape[0], shape[2]
@@ -617,7 +618,7 @@ def run_ours(args, world, rank, local):
     r = measure(args, world, rank, local, full=True)
     torch.cuda.empty_cache()
     c2 = None
-    if args.config == "c3" and world == 1 and not args.no_c2 and args.n is None:
+    if args.config == "c3" and world == 1 and not args.no_c2 and not args.n_override and args.m == 8:
         a2 = copy.copy(args)
         a2.config, a2.nxy, a2.n, a2.nz, a2.m, a2.cfg_name = "c2", 128, 128, 128, 8, "C2 configs[1]"
         a2.steps, a2.warmup = max(args.steps, 200), max(args.warmup, 10)

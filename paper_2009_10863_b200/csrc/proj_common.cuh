@@ -85,30 +85,75 @@ __device__ __forceinline__ double warp_sum(double v) {
     return v;
 }
 
-// Block-reduce NV = MC+1 per-thread values (value MC is a squared norm, slot NORM), write this
-// block's partials to blk[slot*MAXB + blockIdx], and take a ticket.  Returns true in the block
-// that arrived last (it then owns the final, block-ordered reduction).
+// Warp sums of the MC coefficient values by a butterfly reduce-scatter: at xor offset o a lane
+// keeps one half of the values it still holds and receives the partner's partial sums of that
+// half (K/2 shuffles), so MC values cost MC-1 shuffles instead of 5*MC.  Lane l ends up holding
+// the warp sum of value index l / (32/K0) (K0 = MC rounded up to a power of two, K0 <= 32); the
+// fixed xor pattern makes the summation order deterministic.  The norm (value MC) is a plain
+// xor-tree sum.  Inactive values are exact zeros, so they are reduced like the others and only
+// the stores are conditional (no divergent shuffles).
+template <int MC> struct Pow2 {
+    static constexpr int K0 = MC <= 1 ? 1 : MC <= 2 ? 2 : MC <= 4 ? 4 : MC <= 8 ? 8 : MC <= 16 ? 16 : 32;
+};
+template <int MC>
+__device__ __forceinline__ void warp_reduce_scatter(const double (&v)[MC + 1], double &mine, double &norm) {
+    constexpr int K0 = Pow2<MC>::K0;
+    const int lane = threadIdx.x & 31;
+    double w[K0];
+#pragma unroll
+    for (int k = 0; k < K0; ++k) w[k] = (k < MC) ? v[k] : 0.0;
+#pragma unroll
+    for (int L = 0; L < 5; ++L) {
+        const int o = 16 >> L;
+        const int K = K0 >> L;  // values still held before this step (compile-time after unrolling)
+        if (K > 1) {
+            const int h = K / 2;
+            const bool up = (lane & o) != 0;
+#pragma unroll
+            for (int j = 0; j < h; ++j) {
+                const double send = up ? w[j] : w[j + h];
+                const double keep = up ? w[j + h] : w[j];
+                w[j] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+            }
+        } else {
+            w[0] += __shfl_xor_sync(0xffffffffu, w[0], o);
+        }
+    }
+    mine = w[0];
+    norm = warp_sum(v[MC]);
+}
+// Index of the value lane `lane` holds after warp_reduce_scatter<MC>.
+template <int MC> __device__ __forceinline__ int scatter_index(int lane) { return lane / (32 / Pow2<MC>::K0); }
+
+// Block-reduce NV = MC+1 per-thread values (value MC is a squared norm, slot NORM) into this
+// block's partials blk[slot*MAXB + blockIdx] (warp sums in shared memory, then warp-ordered sums).
+template <int NV>
+__device__ __forceinline__ void block_partials_store(const double (&v)[NV], int nc, bool norm, double *blk,
+                                                     double *sh) {
+    constexpr int MC = NV - 1;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    double mine, nrm;
+    warp_reduce_scatter<MC>(v, mine, nrm);
+    const int k = scatter_index<MC>(lane);
+    if (k < MC && (lane % (32 / Pow2<MC>::K0)) == 0) sh[w * NV + k] = mine;
+    if (lane == 0) sh[w * NV + MC] = nrm;
+    __syncthreads();
+    for (int q = threadIdx.x; q < NV; q += blockDim.x) {
+        const bool act = (q < NV - 1) ? (q < nc) : norm;
+        if (act) {
+            double s = 0.0;
+            for (int j = 0; j < nw; ++j) s += sh[j * NV + q];
+            blk[((q < NV - 1) ? q : NORM) * MAXB + blockIdx.x] = s;
+        }
+    }
+}
+
+// As block_partials_store, then take a ticket (one-kernel-per-pass schedule).  Returns true in the
+// block that arrived last (it then owns the final, block-ordered reduction).
 template <int NV>
 __device__ __forceinline__ bool block_partials_ticket(const double (&v)[NV], int nc, bool norm, double *blk,
                                                       unsigned *ticket, double *sh) {
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
-#pragma unroll
-    for (int k = 0; k < NV; ++k) {
-        const bool act = (k < NV - 1) ? (k < nc) : norm;  // warp-uniform
-        if (act) {
-            const double s = warp_sum(v[k]);
-            if (lane == 0) sh[w * NV + k] = s;
-        }
-    }
-    __syncthreads();
-    for (int k = threadIdx.x; k < NV; k += blockDim.x) {
-        const bool act = (k < NV - 1) ? (k < nc) : norm;
-        if (act) {
-            double s = 0.0;
-            for (int j = 0; j < nw; ++j) s += sh[j * NV + k];
-            blk[((k < NV - 1) ? k : NORM) * MAXB + blockIdx.x] = s;
-        }
-    }
+    block_partials_store<NV>(v, nc, norm, blk, sh);
     __threadfence();
     __syncthreads();
     __shared__ unsigned s_ticket;
@@ -119,77 +164,46 @@ __device__ __forceinline__ bool block_partials_ticket(const double (&v)[NV], int
     return last;
 }
 
-// out[slot] = sum over the gridDim.x block partials of that slot, in a fixed order.  The MC+1
-// possible slots (coefficients 0..MC-1, the norm) are dealt to warps round-robin; lane l owns
-// blocks l, l+32, ...; each chunk issues all its loads (up to 8 blocks x JS slots) at once, so
-// <= 256 blocks cost one L2 round trip; then a fixed xor tree.  Deterministic for a given grid.
+// out[slot] = sum over the gridDim.x block partials of that slot, in a fixed order.  Two stages:
+// TPS = THREADS/(MC+1) threads per slot each sum the blocks r, r+TPS, ... (all loads of a chunk in
+// flight: one L2 round trip for <= CHK*TPS blocks), then one thread per slot sums the TPS partials
+// in order (shared memory).  Few registers, so the trip prefetched across a barrier stays resident
+// even at M = 32.  Deterministic for a given grid.  Every thread of the block must call it.
 template <int MC>
 __device__ __forceinline__ void final_reduce(int nc, bool norm, const double *blk, double *out) {
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    constexpr int NW = THREADS / 32;
-    constexpr int JS = (MC + 1 + NW - 1) / NW;
-    constexpr int CH = JS <= 2 ? 8 : 4;  // blocks per lane per round trip (register budget)
+    constexpr int NS = MC + 1;
+    constexpr int TPS = THREADS / NS;
+    constexpr int CHK = NS > 17 ? 24 : 12;
+    __shared__ double s_part[NS * TPS];
+    const int t = threadIdx.x, q = t / TPS, r = t % TPS;
     const int nb = gridDim.x;
-    double s[JS][CH];
+    if (q < NS) {
+        const bool act = (q < MC) ? (q < nc) : norm;
+        double acc = 0.0;
+        if (act) {
+            const double *src = blk + ((q < MC) ? q : NORM) * MAXB;
+            for (int b0 = r; b0 < nb; b0 += CHK * TPS) {
+                double tv[CHK];
 #pragma unroll
-    for (int j = 0; j < JS; ++j)
+                for (int u = 0; u < CHK; ++u) tv[u] = (b0 + u * TPS < nb) ? __ldcg(src + b0 + u * TPS) : 0.0;
 #pragma unroll
-        for (int u = 0; u < CH; ++u) s[j][u] = 0.0;
-    for (int base = lane; base < nb; base += CH * 32) {
-        double t[JS][CH];
-#pragma unroll
-        for (int j = 0; j < JS; ++j) {
-            const int q = w + j * NW;  // compact slot index: q < MC -> coefficient q, q == MC -> norm
-            const bool act = (q < MC) ? (q < nc) : (q == MC && norm);
-            const int k = (q < MC) ? q : NORM;
-#pragma unroll
-            for (int u = 0; u < CH; ++u) {
-                const int bb = base + u * 32;
-                t[j][u] = (act && bb < nb) ? __ldcg(blk + k * MAXB + bb) : 0.0;
+                for (int u = 0; u < CHK; ++u) acc += tv[u];
             }
         }
-#pragma unroll
-        for (int j = 0; j < JS; ++j)
-#pragma unroll
-            for (int u = 0; u < CH; ++u) s[j][u] += t[j][u];
+        s_part[t] = acc;
     }
-#pragma unroll
-    for (int j = 0; j < JS; ++j) {
-        const int q = w + j * NW;
-        const bool act = (q < MC) ? (q < nc) : (q == MC && norm);
-        if (!act) continue;  // warp-uniform
-        double t = (s[j][0] + s[j][1]) + (s[j][2] + s[j][3]);
-        if (CH == 8) t += (s[j][CH > 4 ? 4 : 0] + s[j][CH > 5 ? 5 : 0]) + (s[j][CH > 6 ? 6 : 0] + s[j][CH > 7 ? 7 : 0]);
-        t = warp_sum(t);
-        if (lane == 0) out[(q < MC) ? q : NORM] = t;
+    __syncthreads();
+    if (t < NS) {
+        const bool act = (t < MC) ? (t < nc) : norm;
+        if (act) {
+            double s = s_part[t * TPS];
+            for (int j = 1; j < TPS; ++j) s += s_part[t * TPS + j];
+            out[(t < MC) ? t : NORM] = s;
+        }
     }
 }
 
 // ------------------------------------------------------------------ persistent-kernel helpers
-// Block-reduce NV per-thread values and store this block's partials (no ticket).
-template <int NV>
-__device__ __forceinline__ void block_partials_store(const double (&v)[NV], int nc, bool norm, double *blk,
-                                                     double *sh) {
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
-#pragma unroll
-    for (int k = 0; k < NV; ++k) {
-        const bool act = (k < NV - 1) ? (k < nc) : norm;
-        if (act) {
-            const double s = warp_sum(v[k]);
-            if (lane == 0) sh[w * NV + k] = s;
-        }
-    }
-    __syncthreads();
-    for (int k = threadIdx.x; k < NV; k += blockDim.x) {
-        const bool act = (k < NV - 1) ? (k < nc) : norm;
-        if (act) {
-            double s = 0.0;
-            for (int j = 0; j < nw; ++j) s += sh[j * NV + k];
-            blk[((k < NV - 1) ? k : NORM) * MAXB + blockIdx.x] = s;
-        }
-    }
-}
-
 __device__ __forceinline__ unsigned ld_acquire_u32(const unsigned *p) {
     unsigned v;
     asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
