@@ -41,10 +41,12 @@ def _stale(target: str, deps) -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(verbose: bool = False, force: bool = False, trace: bool = False) -> str:
+def build(verbose: bool = False, force: bool = False, trace: bool = False, extra_flags=(), out: str | None = None) -> str:
+    """extra_flags / out: experiment builds (A/B of table entries) into another library file."""
     os.makedirs(BUILD, exist_ok=True)
     nvcc = _nvcc()
-    flags = FLAGS + (TRACE_FLAGS if trace else [])
+    flags = FLAGS + (TRACE_FLAGS if trace else []) + list(extra_flags)
+    lib_path = out or LIB
     # objects built with other flags (e.g. an IG_TRACE=1 debug build) are never reused
     stamp = os.path.join(BUILD, "flags.txt")
     want = " ".join(ARCH + flags)
@@ -74,16 +76,16 @@ def build(verbose: bool = False, force: bool = False, trace: bool = False) -> st
         for s in ex.map(run, jobs):
             if verbose:
                 print("compiled", os.path.relpath(s, ROOT))
-    if force or jobs or _stale(LIB, objs):
-        cmd = [nvcc, *ARCH, "-shared", "-cudart", "static", "-o", LIB, *objs, "-ldl", "-lpthread", "-lrt"]
+    if force or jobs or _stale(lib_path, objs):
+        cmd = [nvcc, *ARCH, "-shared", "-cudart", "static", "-o", lib_path, *objs, "-ldl", "-lpthread", "-lrt"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")
         if verbose:
-            print("linked", os.path.relpath(LIB, ROOT))
+            print("linked", os.path.relpath(lib_path, ROOT))
     with open(stamp, "w") as f:
         f.write(want)
-    return LIB
+    return lib_path
 
 
 if __name__ == "__main__":

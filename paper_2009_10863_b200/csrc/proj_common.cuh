@@ -95,13 +95,16 @@ __device__ __forceinline__ double warp_sum(double v) {
 template <int MC> struct Pow2 {
     static constexpr int K0 = MC <= 1 ? 1 : MC <= 2 ? 2 : MC <= 4 ? 4 : MC <= 8 ? 8 : MC <= 16 ? 16 : 32;
 };
+// Works in place: v[0..MC-1] are clobbered (the callers' accumulators are dead afterwards).
 template <int MC>
-__device__ __forceinline__ void warp_reduce_scatter(const double (&v)[MC + 1], double &mine, double &norm) {
+__device__ __forceinline__ void warp_reduce_scatter(double (&v)[MC + 1], double &mine, double &norm) {
     constexpr int K0 = Pow2<MC>::K0;
     const int lane = threadIdx.x & 31;
-    double w[K0];
+    norm = warp_sum(v[MC]);
+    double *w = v;  // K0 <= MC whenever K0 > 1 is padded below: use a zero pad slot for MC < K0
+    double pad[K0 > MC ? K0 - MC : 1];
 #pragma unroll
-    for (int k = 0; k < K0; ++k) w[k] = (k < MC) ? v[k] : 0.0;
+    for (int k = 0; k < (K0 > MC ? K0 - MC : 1); ++k) pad[k] = 0.0;
 #pragma unroll
     for (int L = 0; L < 5; ++L) {
         const int o = 16 >> L;
@@ -111,8 +114,9 @@ __device__ __forceinline__ void warp_reduce_scatter(const double (&v)[MC + 1], d
             const bool up = (lane & o) != 0;
 #pragma unroll
             for (int j = 0; j < h; ++j) {
-                const double send = up ? w[j] : w[j + h];
-                const double keep = up ? w[j + h] : w[j];
+                const double hi = (j + h < MC) ? w[j + h] : pad[(j + h - MC) < 0 ? 0 : (j + h - MC)];
+                const double send = up ? w[j] : hi;
+                const double keep = up ? hi : w[j];
                 w[j] = keep + __shfl_xor_sync(0xffffffffu, send, o);
             }
         } else {
@@ -120,7 +124,6 @@ __device__ __forceinline__ void warp_reduce_scatter(const double (&v)[MC + 1], d
         }
     }
     mine = w[0];
-    norm = warp_sum(v[MC]);
 }
 // Index of the value lane `lane` holds after warp_reduce_scatter<MC>.
 template <int MC> __device__ __forceinline__ int scatter_index(int lane) { return lane / (32 / Pow2<MC>::K0); }
@@ -128,8 +131,7 @@ template <int MC> __device__ __forceinline__ int scatter_index(int lane) { retur
 // Block-reduce NV = MC+1 per-thread values (value MC is a squared norm, slot NORM) into this
 // block's partials blk[slot*MAXB + blockIdx] (warp sums in shared memory, then warp-ordered sums).
 template <int NV>
-__device__ __forceinline__ void block_partials_store(const double (&v)[NV], int nc, bool norm, double *blk,
-                                                     double *sh) {
+__device__ __forceinline__ void block_partials_store(double (&v)[NV], int nc, bool norm, double *blk, double *sh) {
     constexpr int MC = NV - 1;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
     double mine, nrm;
@@ -151,7 +153,7 @@ __device__ __forceinline__ void block_partials_store(const double (&v)[NV], int 
 // As block_partials_store, then take a ticket (one-kernel-per-pass schedule).  Returns true in the
 // block that arrived last (it then owns the final, block-ordered reduction).
 template <int NV>
-__device__ __forceinline__ bool block_partials_ticket(const double (&v)[NV], int nc, bool norm, double *blk,
+__device__ __forceinline__ bool block_partials_ticket(double (&v)[NV], int nc, bool norm, double *blk,
                                                       unsigned *ticket, double *sh) {
     block_partials_store<NV>(v, nc, norm, blk, sh);
     __threadfence();
@@ -427,12 +429,63 @@ template <int MC> struct Coef {
 //   U        update pass 1 (B~ rotation + c1)    M=8: 2 -> 208.5, 3 -> 210.7
 //   U2       update pass 2 (mostly L2 hits)      M=8: 1 -> 214.2, 2 -> 208.5, 3 -> 209.1
 //   U3       update pass 3 (X~ pass, 2d+2 streams)
+// Elements per trip by bucket for MC <= 4 (U: update pass 1, U2: pass 2, U3: pass 3, P1/P2: form
+// passes): few streams need more rows per trip for enough bytes in flight (A/B at N = 2^27:
+// QR(1) 1.028 -> 1.094, QR(2) 0.967 -> 1.047, QR(4) 1.040 -> 1.052 of the copy roofline; N = 1e7:
+// QR(2) 0.923 -> 0.995).  Experiment builds override single entries with -DIG_T_<FIELD>_<MC>=v
+// (scripts/build_variants.py); the default build uses these values.
+#define IG_T(F, MC, V) (MC == 1 ? IG_T_##F##_1 : MC == 2 ? IG_T_##F##_2 : MC == 4 ? IG_T_##F##_4 : V)
+#ifndef IG_T_U_1
+#define IG_T_U_1 8
+#endif
+#ifndef IG_T_U_2
+#define IG_T_U_2 6
+#endif
+#ifndef IG_T_U_4
+#define IG_T_U_4 4
+#endif
+#ifndef IG_T_U2_1
+#define IG_T_U2_1 4
+#endif
+#ifndef IG_T_U2_2
+#define IG_T_U2_2 8
+#endif
+#ifndef IG_T_U2_4
+#define IG_T_U2_4 6
+#endif
+#ifndef IG_T_U3_1
+#define IG_T_U3_1 6
+#endif
+#ifndef IG_T_U3_2
+#define IG_T_U3_2 4
+#endif
+#ifndef IG_T_U3_4
+#define IG_T_U3_4 2
+#endif
+#ifndef IG_T_P1_1
+#define IG_T_P1_1 8
+#endif
+#ifndef IG_T_P1_2
+#define IG_T_P1_2 6
+#endif
+#ifndef IG_T_P1_4
+#define IG_T_P1_4 4
+#endif
+#ifndef IG_T_P2_1
+#define IG_T_P2_1 8
+#endif
+#ifndef IG_T_P2_2
+#define IG_T_P2_2 8
+#endif
+#ifndef IG_T_P2_4
+#define IG_T_P2_4 6
+#endif
 template <int MC> struct FusedUnroll {
-    static constexpr int U = MC <= 4 ? 4 : (MC <= 8 ? 2 : 1);
-    static constexpr int U3 = MC <= 2 ? 4 : (MC <= 4 ? 2 : 1);
-    static constexpr int U2 = MC <= 4 ? 4 : (MC <= 8 ? 2 : 1);
-    static constexpr int FORM_P1 = MC == 8 ? 3 : U;
-    static constexpr int FORM_P2 = MC == 8 ? 3 : U;
+    static constexpr int U = IG_T(U, MC, (MC <= 8 ? 2 : 1));
+    static constexpr int U3 = IG_T(U3, MC, 1);
+    static constexpr int U2 = IG_T(U2, MC, (MC <= 8 ? 2 : 1));
+    static constexpr int FORM_P1 = IG_T(P1, MC, (MC == 8 ? 3 : 1));
+    static constexpr int FORM_P2 = IG_T(P2, MC, (MC == 8 ? 3 : 1));
     static constexpr int FORM_PF = MC == 8 ? 1 : (MC < 8 ? 2 : 1);
     // For MC >= 16 the per-column coefficients (c1, c2, Givens c/s) are read from shared memory
     // at each use instead of living in 4*MC registers, which the column loads need.
