@@ -96,23 +96,28 @@ def main():
     ap.add_argument("--full")
     ap.add_argument("--bench")
     ap.add_argument("--tag", default="r1")
-    ap.add_argument("--M", type=int, default=8)
-    ap.add_argument("--N", type=int, default=128 ** 3)
+    ap.add_argument("--M", type=int, default=None, help="default: the bench line's history_m (else 8)")
+    ap.add_argument("--N", type=int, default=None, help="default: the bench line's dofs_per_gpu (else 128^3)")
     a = ap.parse_args()
     prof = os.path.join(ROOT, "profiles")
     os.makedirs(prof, exist_ok=True)
-    md = [f"# ncu summary `{a.tag}` (B200, bench.py C2: N = {a.N} DOFs, M = {a.M})", ""]
-    vb = 8 * a.N
-    M = a.M
-    alg = {"form_dot": (M + 1) * vb, "form_combine": (M + 1) * vb, "u1": 2 * M * vb, "u2": M * vb,
-           "u3": (3 * M + 2) * vb, "extrap": (M + 1) * vb, "copy": 2 * vb, "form_fused": 2 * (M + 1) * vb,
-           "update_fused": (6 * M + 2) * vb}
+    bench_line, nnz = None, None
     if a.bench and os.path.exists(a.bench):
         lines = [l for l in open(a.bench).read().splitlines() if l.startswith("{")]
         if lines:
-            b = json.loads(lines[-1])
-            md += ["## bench.py line (same build)", "", "```json", json.dumps(b, indent=1)[:6000], "```", ""]
-            shutil.copy(a.bench, os.path.join(prof, f"{a.tag}_bench.json"))
+            bench_line = json.loads(lines[-1])
+    cfg = (bench_line or {}).get("config", {})
+    N = a.N or cfg.get("dofs_per_gpu") or 128 ** 3
+    M = a.M or cfg.get("history_m") or 8
+    nnz = cfg.get("extrap_nnz") or M  # extrapolation streams the nonzero weights only
+    md = [f"# ncu summary `{a.tag}` (B200, bench.py {cfg.get('workload', 'C2').split(':')[0]}: N = {N} DOFs, M = {M})", ""]
+    vb = 8 * N
+    alg = {"form_dot": (M + 1) * vb, "form_combine": (M + 1) * vb, "u1": 2 * M * vb, "u2": M * vb,
+           "u3": (3 * M + 2) * vb, "extrap": (nnz + 1) * vb, "copy": 2 * vb, "form_fused": 2 * (M + 1) * vb,
+           "update_fused": (6 * M + 2) * vb}
+    if bench_line is not None:
+        md += ["## bench.py line (same build)", "", "```json", json.dumps(bench_line, indent=1)[:6000], "```", ""]
+        shutil.copy(a.bench, os.path.join(prof, f"{a.tag}_bench.json"))
     if a.launches and os.path.exists(a.launches):
         shutil.copy(a.launches, os.path.join(prof, f"{a.tag}_launches.csv"))
         L = read_launches(a.launches)
@@ -150,7 +155,7 @@ def main():
                       f"{d['launch__registers_per_thread'][0]} | {d['launch__grid_size'][0]} |")
             seen.setdefault(k, []).append(rd + wr)
         for k, v in seen.items():
-            traffic[f"{k}@M{a.M}N{a.N}"] = sum(v) / len(v)
+            traffic[f"{k}@M{M}N{N}"] = sum(v) / len(v)
         json.dump(traffic, open(tpath, "w"), indent=1, sort_keys=True)
         md.append("")
         shutil.copy(a.full, os.path.join(prof, f"{a.tag}_full.ncu-rep"))
