@@ -176,6 +176,45 @@ int ig_update_batch_host(int n, ig_t *handles, const double *const *xs, const do
  * ig_form_guess).  NULL for projection methods. */
 double *ig_next_slot(ig_t h);
 
+/* ---------------------------------------------------------------- captured time steps */
+
+/* Device-resident extrapolation window (the per-field history spaces of
+ * PAPER.md:903-907, the zero-cost push of PAPER.md:1817-1819).  By default the window position
+ * (head, fill) lives on the host and every ig_form_guess passes the weights and the solution
+ * pointers of the current fill by value -- the fastest form for eager calls, but a captured CUDA
+ * graph would replay the pointers of the capture step.  on = 1 moves the position into device
+ * memory (a push counter): the extrapolation kernel reads f = min(pushes, M), picks the f stored
+ * solutions and the warm-up weights of that f (Eq. LSQRCOEFFS table, nonzero weights only) on
+ * the device, and the push kernel writes the solution into slot (pushes mod M) and advances the
+ * counter -- no host state per call, so ig_form_guess / ig_update (single or batched) may be
+ * captured once and replayed every time step.  Same arithmetic and summation order as the host
+ * window (bitwise-identical guesses).  The push copies x unless x already IS the next slot
+ * (zero-copy, e.g. x from ig_next_slot).  Switching either way keeps the history (any time).
+ * Calls that read the window position on the host (ig_next_slot, ig_history_dim, ig_get_stats,
+ * ig_bytes -- which then reports the form at the CURRENT window --, the *_host variants,
+ * ig_save_state) sync the stream while on = 1.  Projection handles need nothing: their state is
+ * always on the device.  IG_E_ARG for a projection handle; IG_E_OOM if the 33 KB table cannot
+ * be allocated.  Capturing an extrapolation call of a handle with a host window returns
+ * IG_E_STATE (it would replay stale pointers). */
+int ig_set_device_ring(ig_t h, int on);
+
+/* Stream capture of a whole time step (all fields' ig_form_guess... / ig_update... calls, and any
+ * other work the caller enqueues on the same stream) into a CUDA graph, replayed with ONE launch
+ * per step: removes the host's per-kernel launch cost, which dominates below ~1e6 DOFs.
+ *   ig_capture_begin(stream): cudaStreamBeginCapture (thread-local mode) on a NON-default stream;
+ *     every handle used in the captured calls must have ig_set_stream(h, stream).
+ *   ig_capture_end(stream, &g): ends the capture and instantiates it; *g = NULL on error.
+ *   ig_graph_launch(g, stream): one replay (asynchronous on `stream`).
+ *   ig_graph_destroy(g): releases it (NULL: no-op).
+ * The captured calls bind the device pointers passed at capture time: each step the caller
+ * writes its new b / x / Ax into those buffers (or solves into them) before the replay.
+ * ig_total_launches() counts the captured libig kernels once per replay, not at capture. */
+typedef struct ig_graph_ctx *ig_graph_t;
+int ig_capture_begin(void *cuda_stream);
+int ig_capture_end(void *cuda_stream, ig_graph_t *out);
+int ig_graph_launch(ig_graph_t g, void *cuda_stream);
+void ig_graph_destroy(ig_graph_t g);
+
 /* ---------------------------------------------------------------- checkpoint / resume */
 
 /* Host-memory image of one history space (B~, X~, R and the device control block for

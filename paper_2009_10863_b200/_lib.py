@@ -70,6 +70,11 @@ _SIGS = {
     "ig_set_launch": (C.c_int, [_P, C.c_int]),
     "ig_set_watchdog": (C.c_int, [_P, C.c_double]),
     "ig_profile_read": (C.c_int, [_P, C.c_int, _D, C.POINTER(C.c_int64)]),
+    "ig_set_device_ring": (C.c_int, [_P, C.c_int]),
+    "ig_capture_begin": (C.c_int, [_P]),
+    "ig_capture_end": (C.c_int, [_P, C.POINTER(_P)]),
+    "ig_graph_launch": (C.c_int, [_P, _P]),
+    "ig_graph_destroy": (None, [_P]),
 }
 
 KERNELS = ["form_dot", "form_combine", "u1", "u2", "u3", "extrap", "copy", "form_fused", "update_fused"]

@@ -180,8 +180,14 @@ struct ig_ctx {
     // extrapolation
     std::vector<std::vector<double>> table;  // table[f-1]: weights for f stored solutions
     std::vector<double *> slots;
-    int head = 0, fill = 0;
+    int head = 0, fill = 0;     // host window (ignored while dring: the device counter rules)
     bool last_copy = false;
+    // device-resident window (ig_set_device_ring): graph-capturable form / push
+    bool dring = false;
+    DevRing *ring = nullptr;
+    RingTab *rtab = nullptr;
+    int ring_fc = 0;            // max nonzero weights over every fill (kernel bucket)
+    RingTab rtab_host;
     int last_form_f = 0;
     // host staging (end-to-end path)
     double *stage[4] = {nullptr, nullptr, nullptr, nullptr};
@@ -238,7 +244,9 @@ struct Prof {
     int kid;
     cudaEvent_t a = nullptr;
     Prof(ig_t h_, int kid_) : h(h_), kid(kid_) {
-        if (h->profiling) {
+        cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+        if (h->profiling && cudaStreamIsCapturing(h->stream, &cap) != cudaSuccess) cudaGetLastError();
+        if (h->profiling && cap == cudaStreamCaptureStatusNone) {  // events cannot time a capture
             a = pool_get(h);
             cudaEventRecord(a, h->stream);
         }
@@ -381,6 +389,50 @@ bool extrap_args(ig_t h, double *x0, ExtrapArgs &a, bool &aligned) {
 }
 double *next_slot_ptr(ig_t h) { return h->fill < h->M ? h->slots[slot_index(h, h->fill)] : h->slots[h->head]; }
 
+bool capturing(cudaStream_t s) {
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(s, &cap) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return cap != cudaStreamCaptureStatusNone;
+}
+
+// Device window <-> host window: cnt = fill while filling, M + head once full (cnt mod M = head).
+unsigned long long ring_cnt_of(ig_t h) { return h->fill < h->M ? (unsigned long long)h->fill : (unsigned long long)(h->M + h->head); }
+void ring_set_host(ig_t h, unsigned long long cnt) {
+    h->fill = cnt < (unsigned long long)h->M ? (int)cnt : h->M;
+    h->head = cnt < (unsigned long long)h->M ? 0 : (int)(cnt % (unsigned long long)h->M);
+}
+// Host mirror of a device window (syncs the stream): for the introspection / checkpoint calls.
+int ring_pull(ig_t h) {
+    if (!h->dring) return IG_OK;
+    DevRing r;
+    CUDA_OK(cudaMemcpyAsync(&r, h->ring, sizeof r, cudaMemcpyDeviceToHost, h->stream));
+    CUDA_OK(cudaStreamSynchronize(h->stream));
+    ring_set_host(h, r.cnt);
+    return IG_OK;
+}
+int ring_push_host(ig_t h) {  // host window -> device counter (enqueued; syncs: r is a stack object)
+    if (!h->dring) return IG_OK;
+    DevRing r = {ring_cnt_of(h), 0u, 0u};
+    CUDA_OK(cudaMemcpyAsync(h->ring, &r, sizeof r, cudaMemcpyHostToDevice, h->stream));
+    CUDA_OK(cudaStreamSynchronize(h->stream));
+    return IG_OK;
+}
+bool in_slab(ig_t h, const double *p) { return p >= h->slab && p < h->slab + (size_t)h->M * h->ld; }
+RingArgs ring_args(ig_t h) {
+    RingArgs r;
+    memset(&r, 0, sizeof r);
+    r.ring = h->ring;
+    r.tab = h->rtab;
+    r.base = h->slab;
+    r.ld = h->ld;
+    r.N = h->N;
+    r.M = h->M;
+    return r;
+}
+
 ig_t create_impl(int64_t N, int method, int m, int degree, void *storage, size_t bytes) {
     if (N < 1) return set_err(IG_E_ARG, "N must be >= 1 (got %lld)", (long long)N), nullptr;
     if (!is_proj(method) && !is_extrap(method)) return set_err(IG_E_ARG, "unknown method %d", method), nullptr;
@@ -474,6 +526,8 @@ void ig_destroy(ig_t h) {
     if (h->stream) cudaStreamSynchronize(h->stream);
     else cudaDeviceSynchronize();
     if (h->own_slab) cudaFree(h->slab);
+    cudaFree(h->ring);
+    cudaFree(h->rtab);
     cudaFree(h->ctrl);
     cudaFree(h->blk);
     if (h->gath != h->part) cudaFree(h->gath);
@@ -524,6 +578,7 @@ int ig_reset(ig_t h) {
     }
     h->head = h->fill = 0;
     h->known_d = 0;
+    if (h->dring) CUDA_OK(cudaMemsetAsync(h->ring, 0, sizeof(DevRing), h->stream));
     return IG_OK;
 }
 
@@ -548,6 +603,8 @@ size_t ig_state_bytes(ig_t h) {
 int ig_save_state(ig_t h, void *host_buf, size_t bytes) {
     if (!h || !host_buf || bytes < ig_state_bytes(h)) return set_err(IG_E_ARG, "bad handle or buffer too small");
     DevGuard g(h->dev);
+    int rc = ring_pull(h);
+    if (rc) return rc;
     char *p = static_cast<char *>(host_buf);
     StateHeader hd = {STATE_MAGIC, h->method, h->M, h->degree, h->head, h->N, h->fill, nslabs(h), h->eps};
     memcpy(p, &hd, sizeof hd);
@@ -606,7 +663,7 @@ int ig_load_state(ig_t h, const void *host_buf, size_t bytes) {
     h->head = hd.head;
     h->fill = hd.fill;
     h->eps = hd.eps;
-    return IG_OK;
+    return ring_push_host(h);
 }
 
 int ig_form_guess(ig_t h, const double *b, double *x0) {
@@ -642,6 +699,19 @@ int ig_form_guess(ig_t h, const double *b, double *x0) {
         count(h, 2);
         return IG_OK;
     }
+    if (h->dring) {  // device window: f, slots and weights are read on the device
+        RingBatch rb;
+        memset(&rb, 0, sizeof rb);
+        rb.f[0] = ring_args(h);
+        rb.f[0].x0 = x0;
+        rb.nf = 1;
+        Prof p(h, IG_K_EXTRAP);
+        CUDA_OK(launch_extrap_ring(rb, h->ring_fc, al16(x0) ? 2 : 1, h->nsm, h->stream));
+        count(h, 1);
+        return IG_OK;
+    }
+    if (capturing(h->stream))
+        return set_err(IG_E_STATE, "extrapolation window is host-side: ig_set_device_ring(h, 1) before capturing");
     ExtrapArgs a;
     bool aligned = true;
     if (!extrap_args(h, x0, a, aligned)) return IG_OK;  // fill == 0: x0 untouched (AMB-13)
@@ -693,6 +763,20 @@ int ig_update(ig_t h, const double *x, const double *Ax) {
         count(h, 3);
         return IG_OK;
     }
+    if (h->dring) {  // device window: the push kernel picks the slot and advances the counter
+        RingBatch rb;
+        memset(&rb, 0, sizeof rb);
+        rb.f[0] = ring_args(h);
+        rb.f[0].x = x;
+        rb.nf = 1;
+        h->last_copy = !in_slab(h, x);
+        Prof p(h, IG_K_COPY);
+        CUDA_OK(launch_push_ring(rb, al16(x) ? 2 : 1, h->nsm, h->stream));
+        count(h, 1);
+        return IG_OK;
+    }
+    if (capturing(h->stream))
+        return set_err(IG_E_STATE, "extrapolation window is host-side: ig_set_device_ring(h, 1) before capturing");
     double *slot = next_slot_ptr(h);
     h->last_copy = (x != slot);
     if (h->last_copy) {
@@ -717,6 +801,31 @@ int ig_form_guess_batch(int n, ig_t *hs, const double *const *bs, double *const 
             ++i;
             continue;
         }
+        if (h->dring) {  // consecutive device-window handles on the same device and stream: one launch
+            RingBatch rb;
+            memset(&rb, 0, sizeof rb);
+            int fc = 0;
+            bool aligned = true;
+            int j = i;
+            for (; j < n && rb.nf < MAXF; ++j) {
+                ig_t q = hs[j];
+                if (!q || !is_extrap(q->method) || !q->dring || q->dev != h->dev || q->stream != h->stream) break;
+                if (!x0s[j]) return set_err(IG_E_ARG, "x0 is NULL");
+                rb.f[rb.nf] = ring_args(q);
+                rb.f[rb.nf].x0 = x0s[j];
+                aligned = aligned && al16(x0s[j]);
+                fc = q->ring_fc > fc ? q->ring_fc : fc;
+                ++rb.nf;
+            }
+            DevGuard g(h->dev);
+            Prof p(h, IG_K_EXTRAP);
+            CUDA_OK(launch_extrap_ring(rb, fc, aligned ? 2 : 1, h->nsm, h->stream));
+            count(h, 1);
+            i = j;
+            continue;
+        }
+        if (capturing(h->stream))
+            return set_err(IG_E_STATE, "extrapolation window is host-side: ig_set_device_ring(h, 1) before capturing");
         // group consecutive extrapolation handles on the same device and stream
         ExtrapBatch b;
         memset(&b, 0, sizeof b);
@@ -724,7 +833,7 @@ int ig_form_guess_batch(int n, ig_t *hs, const double *const *bs, double *const 
         int j = i;
         for (; j < n && b.nf < MAXF; ++j) {
             ig_t q = hs[j];
-            if (!q || !is_extrap(q->method) || q->dev != h->dev || q->stream != h->stream) break;
+            if (!q || !is_extrap(q->method) || q->dring || q->dev != h->dev || q->stream != h->stream) break;
             if (!x0s[j]) return set_err(IG_E_ARG, "x0 is NULL");
             bool al = true;
             if (extrap_args(q, x0s[j], b.f[b.nf], al)) {
@@ -745,9 +854,36 @@ int ig_form_guess_batch(int n, ig_t *hs, const double *const *bs, double *const 
 
 int ig_update_batch(int n, ig_t *hs, const double *const *xs, const double *const *Axs) {
     if (n < 0 || (n > 0 && (!hs || !xs))) return set_err(IG_E_ARG, "bad batch arguments");
-    for (int i = 0; i < n; ++i) {
-        int rc = ig_update(hs[i], xs[i], Axs ? Axs[i] : nullptr);
-        if (rc) return rc;
+    int i = 0;
+    while (i < n) {
+        ig_t h = hs[i];
+        if (!h) return set_err(IG_E_ARG, "NULL handle in batch");
+        if (!is_extrap(h->method) || !h->dring) {
+            int rc = ig_update(h, xs[i], Axs ? Axs[i] : nullptr);
+            if (rc) return rc;
+            ++i;
+            continue;
+        }
+        // consecutive device-window extrapolation handles (same device and stream): one push launch
+        RingBatch rb;
+        memset(&rb, 0, sizeof rb);
+        bool aligned = true;
+        int j = i;
+        for (; j < n && rb.nf < MAXF; ++j) {
+            ig_t q = hs[j];
+            if (!q || !is_extrap(q->method) || !q->dring || q->dev != h->dev || q->stream != h->stream) break;
+            if (!xs[j]) return set_err(IG_E_ARG, "x is NULL");
+            rb.f[rb.nf] = ring_args(q);
+            rb.f[rb.nf].x = xs[j];
+            q->last_copy = !in_slab(q, xs[j]);
+            aligned = aligned && al16(xs[j]);
+            ++rb.nf;
+        }
+        DevGuard g(h->dev);
+        Prof p(h, IG_K_COPY);
+        CUDA_OK(launch_push_ring(rb, aligned ? 2 : 1, h->nsm, h->stream));
+        count(h, 1);
+        i = j;
     }
     return IG_OK;
 }
@@ -810,6 +946,8 @@ int ig_form_guess_host(ig_t h, const double *b, double *x0) {
         rc = ig_form_guess(h, h->stage[0], h->stage[1]);
         if (rc) return rc;
     } else {
+        rc = ring_pull(h);
+        if (rc) return rc;
         if (h->fill == 0) return IG_OK;  // x0 untouched, nothing to move
         rc = ig_form_guess(h, nullptr, h->stage[1]);
         if (rc) return rc;
@@ -836,6 +974,8 @@ int ig_update_host(ig_t h, const double *x, const double *Ax) {
         CUDA_OK(cudaStreamSynchronize(h->stream));
         return ctrl_consume(h);
     }
+    int rc0 = ring_pull(h);
+    if (rc0) return rc0;
     double *slot = next_slot_ptr(h);  // copy straight into the ring slot: zero-copy push
     CUDA_OK(cudaMemcpyAsync(slot, x, nb, cudaMemcpyHostToDevice, h->stream));
     int rc = ig_update(h, slot, nullptr);
@@ -855,6 +995,7 @@ int ig_form_guess_batch_host(int n, ig_t *hs, const double *const *bs, double *c
         int rc = ensure_stage(hs[i]);
         if (!rc) rc = ensure_cstream(hs[i]);
         if (!rc && is_proj(hs[i]->method)) rc = known_dim(hs[i]);
+        if (!rc) rc = ring_pull(hs[i]);
         if (rc) return rc;
     }
     // 1) extrapolation fields first (no inputs): kernel on the handle's stream, D2H of the guess on
@@ -898,6 +1039,7 @@ int ig_update_batch_host(int n, ig_t *hs, const double *const *xs, const double 
         DevGuard g(hs[i]->dev);
         int rc = ensure_stage(hs[i]);
         if (!rc) rc = ensure_cstream(hs[i]);
+        if (!rc) rc = ring_pull(hs[i]);
         if (rc) return rc;
     }
     // 1) projection fields: H2D x, Ax, then the update kernel
@@ -947,6 +1089,10 @@ int ig_update_batch_host(int n, ig_t *hs, const double *const *xs, const double 
 
 double *ig_next_slot(ig_t h) {
     if (!h || !is_extrap(h->method)) return nullptr;
+    if (h->dring) {
+        DevGuard g(h->dev);
+        if (ring_pull(h)) return nullptr;
+    }
     return next_slot_ptr(h);
 }
 
@@ -1112,6 +1258,96 @@ static int watchdog_error(int err) {
     return IG_OK;
 }
 
+int ig_set_device_ring(ig_t h, int on) {
+    if (!h || !is_extrap(h->method)) return set_err(IG_E_ARG, "extrapolation handle required");
+    DevGuard g(h->dev);
+    if (on && !h->dring) {
+        if (!h->ring) {
+            RingTab &t = h->rtab_host;
+            memset(&t, 0, sizeof t);
+            int fc = 0;
+            for (int f = 1; f <= h->M; ++f) {
+                int nz = 0;
+                for (int j = 0; j < f; ++j) {
+                    const double bj = h->table[f - 1][j];
+                    if (bj == 0.0) continue;  // zero weights are not streamed (as extrap_args)
+                    t.jidx[f - 1][nz] = j;
+                    t.beta[f - 1][nz] = bj;
+                    ++nz;
+                }
+                t.nnz[f - 1] = nz;
+                fc = nz > fc ? nz : fc;
+            }
+            h->ring_fc = fc;
+            if (cudaMalloc(&h->ring, sizeof(DevRing)) != cudaSuccess || cudaMalloc(&h->rtab, sizeof(RingTab)) != cudaSuccess) {
+                cudaGetLastError();
+                cudaFree(h->ring);
+                h->ring = nullptr;
+                return set_err(IG_E_OOM, "device window allocation failed");
+            }
+            CUDA_OK(cudaMemcpyAsync(h->rtab, &t, sizeof t, cudaMemcpyHostToDevice, h->stream));
+        }
+        h->dring = true;
+        return ring_push_host(h);  // the device counter continues the host window
+    }
+    if (!on && h->dring) {
+        int rc = ring_pull(h);
+        if (rc) return rc;
+        h->dring = false;
+    }
+    return IG_OK;
+}
+
+struct ig_graph_ctx {
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    int64_t launches = 0;  // libig kernels per replay
+};
+static thread_local int64_t g_capture_launches0 = 0;
+
+int ig_capture_begin(void *stream) {
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (!s) return set_err(IG_E_ARG, "capture needs a non-default stream");
+    CUDA_OK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+    g_capture_launches0 = g_launches.load();
+    return IG_OK;
+}
+
+int ig_capture_end(void *stream, ig_graph_t *out) {
+    if (!out) return set_err(IG_E_ARG, "NULL out");
+    *out = nullptr;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    cudaGraph_t graph = nullptr;
+    CUDA_OK(cudaStreamEndCapture(s, &graph));
+    ig_graph_ctx *g = new ig_graph_ctx;
+    g->graph = graph;
+    // the captured calls counted their launches; they run at every replay instead
+    g->launches = g_launches.load() - g_capture_launches0;
+    g_launches -= g->launches;
+    if (cudaGraphInstantiateWithFlags(&g->exec, graph, 0) != cudaSuccess) {
+        cudaError_t e = cudaGetLastError();
+        cudaGraphDestroy(graph);
+        delete g;
+        return set_err(IG_E_CUDA, "cudaGraphInstantiate: %s", cudaGetErrorString(e));
+    }
+    *out = g;
+    return IG_OK;
+}
+
+int ig_graph_launch(ig_graph_t g, void *stream) {
+    if (!g) return set_err(IG_E_ARG, "NULL graph");
+    CUDA_OK(cudaGraphLaunch(g->exec, static_cast<cudaStream_t>(stream)));
+    g_launches += g->launches;
+    return IG_OK;
+}
+
+void ig_graph_destroy(ig_graph_t g) {
+    if (!g) return;
+    if (g->exec) cudaGraphExecDestroy(g->exec);
+    if (g->graph) cudaGraphDestroy(g->graph);
+    delete g;
+}
+
 int ig_history_dim(ig_t h, int *d) {
     if (!h || !d) return set_err(IG_E_ARG, "NULL argument");
     DevGuard g(h->dev);
@@ -1122,6 +1358,8 @@ int ig_history_dim(ig_t h, int *d) {
         *d = c.d;
         return watchdog_error(c.err);
     } else {
+        int rc = ring_pull(h);
+        if (rc) return rc;
         *d = h->fill;
     }
     return IG_OK;
@@ -1152,6 +1390,8 @@ int ig_get_stats(ig_t h, ig_stats_t *out) {
         out->norm_bt = c.nb;
         if (c.err) return watchdog_error(c.err);
     } else {
+        int rc = ring_pull(h);
+        if (rc) return rc;
         out->d = h->fill;
         out->admitted = 1;
     }
@@ -1163,6 +1403,11 @@ int ig_bytes(ig_t h, int64_t *form_bytes, int64_t *update_bytes) {
     DevGuard g(h->dev);
     const int64_t vb = 8 * h->N;
     if (is_extrap(h->method)) {
+        if (h->dring) {  // device window: the form at the current window (the host never saw f)
+            int rc = ring_pull(h);
+            if (rc) return rc;
+            h->last_form_f = h->fill > 0 ? h->rtab_host.nnz[h->fill - 1] : 0;
+        }
         *form_bytes = h->last_form_f ? (h->last_form_f + 1) * vb : 0;
         *update_bytes = h->last_copy ? 2 * vb : 0;
         return IG_OK;

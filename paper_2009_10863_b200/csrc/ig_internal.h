@@ -98,6 +98,38 @@ struct ExtrapBatch {
     int nf;
 };
 
+// Device-resident solution window (ig_set_device_ring): the push counter lives in device memory
+// and the kernels derive the window from it, so form/push calls carry no host-side state and can
+// be captured once into a CUDA graph and replayed every time step.
+//   cnt = solutions pushed so far; f = min(cnt, M) stored; the j-th oldest (j = 0..f-1) is in
+//   slot (cnt - f + j) mod M; the next push goes to slot cnt mod M (the same window as the host
+//   ring's head/fill: head = cnt mod M once full).
+struct DevRing {
+    unsigned long long cnt;
+    unsigned ticket;  // CTAs of the running push that have read cnt (the last one advances it)
+    unsigned pad_;
+};
+struct RingTab {      // per fill f = 1..M (row f-1): the nonzero weights, oldest first
+    int nnz[MAXM];
+    int jidx[MAXM][MAXM];
+    double beta[MAXM][MAXM];
+};
+struct RingArgs {
+    DevRing *ring;
+    const RingTab *tab;
+    double *base;      // slot k at base + k*ld
+    int64_t ld;
+    int64_t N;
+    int M;
+    int pad_;
+    double *x0;        // form: guess (out)
+    const double *x;   // push: solution (in)
+};
+struct RingBatch {
+    RingArgs f[MAXF];
+    int nf;
+};
+
 // ----------------------------------------------------------------------------- launch policy
 // Process-wide launch defaults (env IG_LAUNCH, comma list of "coop", "plain", "pdl", "nopdl";
 // default coop + pdl; a handle overrides the coop choice with ig_set_launch):
@@ -159,6 +191,10 @@ cudaError_t launch_update_fused(const ProjArgs &a, int vec, int nsm, cudaStream_
 cudaError_t launch_extrap(const ExtrapArgs &a, int vec, int nsm, cudaStream_t s);
 cudaError_t launch_extrap_batch(const ExtrapBatch &b, int vec, int nsm, cudaStream_t s);
 cudaError_t launch_copy(double *dst, const double *src, int64_t N, int vec, int nsm, cudaStream_t s);
+// Device-ring extrapolation (one launch for up to MAXF fields; fc = max nonzero weights over all
+// fills of all fields, so the launch never depends on the current fill).
+cudaError_t launch_extrap_ring(const RingBatch &b, int fc, int vec, int nsm, cudaStream_t s);
+cudaError_t launch_push_ring(const RingBatch &b, int vec, int nsm, cudaStream_t s);
 
 // Cached cudaOccupancyMaxActiveBlocksPerMultiprocessor(kernel, THREADS) (api.cpp); the query is
 // ~microseconds of host time, paid once per kernel instantiation instead of per launch.

@@ -76,8 +76,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_extrap_batch(const __grid_consta
 }
 
 template <int VEC, int U>
-__global__ void __launch_bounds__(THREADS, 1) k_copy(double *__restrict__ dst, const double *__restrict__ src, int64_t N) {
-    pdl_wait();
+__device__ __forceinline__ void copy_body(double *__restrict__ dst, const double *__restrict__ src, int64_t N) {
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     if (VEC == 2) {  // U strided 16-byte loads in flight per thread, then the U stores
         const int64_t nv = N >> 1;
@@ -94,6 +93,63 @@ __global__ void __launch_bounds__(THREADS, 1) k_copy(double *__restrict__ dst, c
         if ((N & 1) && blockIdx.x == 0 && threadIdx.x == 0) dst[N - 1] = src[N - 1];
     } else {
         for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < N; i += stride) dst[i] = src[i];
+    }
+}
+
+template <int VEC, int U>
+__global__ void __launch_bounds__(THREADS, 1) k_copy(double *__restrict__ dst, const double *__restrict__ src, int64_t N) {
+    pdl_wait();
+    copy_body<VEC, U>(dst, src, N);
+}
+
+// ----------------------------------------------------------------------------- device ring
+// Same arithmetic as k_extrap / k_copy; the window (f, slot pointers, weights) is derived on the
+// device from the push counter (DevRing), so a captured graph replays correctly at every fill.
+template <int FC, int VEC, int UNROLL>
+__global__ void __launch_bounds__(THREADS, 1) k_extrap_ring(const __grid_constant__ RingBatch b) {
+    pdl_wait();
+    __shared__ ExtrapArgs sa;
+    const RingArgs &r = b.f[blockIdx.y];
+    if (threadIdx.x < 32) {
+        const unsigned long long cnt = *reinterpret_cast<volatile unsigned long long *>(&r.ring->cnt);
+        const int f = cnt < (unsigned long long)r.M ? (int)cnt : r.M;
+        const int nz = f > 0 ? r.tab->nnz[f - 1] : 0;
+        const int lane = threadIdx.x;
+        if (lane < nz) {
+            const int j = r.tab->jidx[f - 1][lane];
+            const int64_t slot = (int64_t)((cnt - (unsigned long long)f + (unsigned long long)j) % (unsigned long long)r.M);
+            sa.src[lane] = r.base + slot * r.ld;
+            sa.beta[lane] = r.tab->beta[f - 1][lane];
+        }
+        if (lane == 0) {
+            sa.f = nz;
+            sa.N = r.N;
+            sa.x0 = r.x0;
+        }
+    }
+    __syncthreads();
+    if (sa.f > 0) extrap_body<FC, VEC, UNROLL>(sa);  // f == 0: x0 untouched (AMB-13)
+    pdl_trigger();
+}
+
+template <int VEC, int U>
+__global__ void __launch_bounds__(THREADS, 1) k_push_ring(const __grid_constant__ RingBatch b) {
+    pdl_wait();
+    const RingArgs &r = b.f[blockIdx.y];
+    __shared__ unsigned long long cnt_s;
+    if (threadIdx.x == 0) cnt_s = *reinterpret_cast<volatile unsigned long long *>(&r.ring->cnt);
+    __syncthreads();
+    const unsigned long long cnt = cnt_s;
+    double *dst = r.base + (int64_t)(cnt % (unsigned long long)r.M) * r.ld;
+    if (dst != r.x) copy_body<VEC, U>(dst, r.x, r.N);  // solved in place: 0 bytes
+    pdl_trigger();
+    if (threadIdx.x == 0) {
+        // every CTA has read cnt before it takes a ticket: the last one advances the window
+        const unsigned t = atomicAdd(&r.ring->ticket, 1u);
+        if (t == gridDim.x - 1) {
+            r.ring->ticket = 0;
+            r.ring->cnt = cnt + 1;
+        }
     }
 }
 
@@ -187,6 +243,56 @@ cudaError_t launch_copy(double *dst, const double *src, int64_t N, int vec, int 
     } else {
         auto k = k_copy<1, 1>;
         launch_ex(k, grid_for_x(k, N, nsm), s, false, dst, src, N);
+    }
+    return cudaGetLastError();
+}
+
+template <class K> static void launch_ring(K kern, const RingBatch &b, int64_t nv, int nsm, cudaStream_t s) {
+    const LaunchFlags fl = launch_flags();
+    cudaLaunchConfig_t cfg = {};
+    int gx = grid_for_x(kern, nv, nsm);
+    gx = (gx + b.nf - 1) / b.nf;  // the fields share the SMs
+    cfg.gridDim = dim3(gx < 1 ? 1 : gx, b.nf);
+    cfg.blockDim = dim3(THREADS);
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = fl.pdl ? 1 : 0;
+    cudaLaunchKernelEx(&cfg, kern, b);
+}
+
+static int64_t ring_nmax(const RingBatch &b) {
+    int64_t nmax = 0;
+    for (int j = 0; j < b.nf; ++j) nmax = b.f[j].N > nmax ? b.f[j].N : nmax;
+    return nmax;
+}
+
+template <int FC>
+static void launch_ring_fc(const RingBatch &b, int vec, int nsm, cudaStream_t s) {
+    const int64_t nmax = ring_nmax(b);
+    if (vec == 2) launch_ring(k_extrap_ring<FC, 2, ExtrapTune<FC>::U>, b, nmax / 2, nsm, s);
+    else launch_ring(k_extrap_ring<FC, 1, (FC <= 2 ? 4 : (FC <= 4 ? 2 : 1))>, b, nmax, nsm, s);
+}
+
+cudaError_t launch_extrap_ring(const RingBatch &b, int fc, int vec, int nsm, cudaStream_t s) {
+    if (fc <= 1) launch_ring_fc<1>(b, vec, nsm, s);
+    else if (fc <= 2) launch_ring_fc<2>(b, vec, nsm, s);
+    else if (fc <= 4) launch_ring_fc<4>(b, vec, nsm, s);
+    else if (fc <= 8) launch_ring_fc<8>(b, vec, nsm, s);
+    else if (fc <= 16) launch_ring_fc<16>(b, vec, nsm, s);
+    else launch_ring_fc<32>(b, vec, nsm, s);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_push_ring(const RingBatch &b, int vec, int nsm, cudaStream_t s) {
+    const int64_t nmax = ring_nmax(b);
+    if (vec == 2) {
+        if (nmax >= (int64_t(1) << 24)) launch_ring(k_push_ring<2, 4>, b, nmax / 2, nsm, s);
+        else launch_ring(k_push_ring<2, 1>, b, nmax / 2, nsm, s);
+    } else {
+        launch_ring(k_push_ring<1, 1>, b, nmax, nsm, s);
     }
     return cudaGetLastError();
 }

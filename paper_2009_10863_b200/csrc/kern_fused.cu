@@ -299,7 +299,9 @@ __global__ void __launch_bounds__(THREADS, 1) k_update_fused(ProjArgs a) {
         const int64_t nh = (pend || newcol) ? Ts : 0;  // the planner's trips 0..Ts-1
         if (planner) {
             TRACE(10);
-            r_update_plan(c, M, deff, pend, newcol, plan, s_r1, s_r2, s_nb, s_R, s_W);
+            r_update(c, M, deff, pend, newcol, s_r1, s_r2, s_nb, s_R);
+            TRACE(13);
+            if (plan) givens_plan(c, M, s_R, s_W);
             TRACE(11);
         } else {
             if (Ts > 0) {

@@ -680,10 +680,9 @@ static __device__ __noinline__ void givens_plan(Ctrl *c, int M, const double *R,
 
 // One warp: R after this update -- its leading M x M block is the downdated R (if a downdate ran)
 // plus, if the pair was admitted, the new column (c1 + c2; ||b~||) (Alg. 2) -- stored
-// to c->R and to sR (shared), then the Givens plan of the next downdate from sR.
-static __device__ __noinline__ void r_update_plan(Ctrl *c, int M, int deff, bool pend, bool newcol, bool plan,
-                                                  const double *r1, const double *r2, double nb, double *sR,
-                                                  double *sW) {
+// to c->R and to sR (shared); the caller then runs givens_plan from sR if the next update downdates.
+static __device__ __noinline__ void r_update(Ctrl *c, int M, int deff, bool pend, bool newcol, const double *r1,
+                                             const double *r2, double nb, double *sR) {
     const int lane = threadIdx.x & 31;
     const double *Rsrc = pend ? c->Rdn : c->R;
 #pragma unroll 1
@@ -697,7 +696,6 @@ static __device__ __noinline__ void r_update_plan(Ctrl *c, int M, int deff, bool
     if (newcol)
         for (int k = M + lane; k < MAXM; k += 32) c->R[k + deff * MAXM] = 0.0;
     __syncwarp();  // sR complete
-    if (plan) givens_plan(c, M, sR, sW);
 }
 
 }  // namespace ig

@@ -314,6 +314,65 @@ def ig_set_launch(h, cooperative: int) -> None:
     _check(lib().ig_set_launch(h, int(cooperative)), "ig_set_launch")
 
 
+def ig_set_device_ring(h, on: bool) -> None:
+    """Extrapolation window position in device memory: graph-capturable form / push (ig.h)."""
+    _check(lib().ig_set_device_ring(h, 1 if on else 0), "ig_set_device_ring")
+
+
+def ig_capture_begin(stream) -> None:
+    _check(lib().ig_capture_begin(C.c_void_p(stream.cuda_stream)), "ig_capture_begin")
+
+
+def ig_capture_end(stream):
+    out = C.c_void_p()
+    _check(lib().ig_capture_end(C.c_void_p(stream.cuda_stream), C.byref(out)), "ig_capture_end")
+    return out.value
+
+
+def ig_graph_launch(g, stream) -> None:
+    _check(lib().ig_graph_launch(g, C.c_void_p(stream.cuda_stream)), "ig_graph_launch")
+
+
+def ig_graph_destroy(g) -> None:
+    lib().ig_graph_destroy(g)
+
+
+class CapturedStep:
+    """`with CapturedStep(stream) as step:` captures the libig calls issued on `stream` (every
+    handle set to it) into a CUDA graph; `step.replay()` relaunches it (ig_capture_* in ig.h)."""
+
+    def __init__(self, stream):
+        self.stream, self.g = stream, None
+
+    def __enter__(self):
+        ig_capture_begin(self.stream)
+        return self
+
+    def __exit__(self, exc_type, exc, tb):
+        if exc_type is not None:  # end the capture, drop the partial graph
+            try:
+                ig_graph_destroy(ig_capture_end(self.stream))
+            except IGError:
+                pass
+            return False
+        self.g = ig_capture_end(self.stream)
+        return False
+
+    def replay(self) -> None:
+        ig_graph_launch(self.g, self.stream)
+
+    def close(self) -> None:
+        if self.g:
+            ig_graph_destroy(self.g)
+            self.g = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
 def ig_set_watchdog(h, seconds: float) -> None:
     _check(lib().ig_set_watchdog(h, float(seconds)), "ig_set_watchdog")
 
@@ -414,6 +473,12 @@ class InitialGuess:
 
     def update(self, x, Ax=None):
         ig_update(self.h, x, Ax)
+
+    def set_device_ring(self, on: bool = True) -> None:
+        ig_set_device_ring(self.h, on)
+
+    def set_stream(self, stream) -> None:
+        ig_set_stream(self.h, stream)
 
     def next_slot(self):
         """torch view of the extrapolation zero-copy slot."""

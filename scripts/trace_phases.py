@@ -38,8 +38,9 @@ for j, nm in enumerate(names):
     print(f"{nm:14s} min {t[:, j].min():8.1f} med {np.median(t[:, j]):8.1f} max {t[:, j].max():8.1f} us")
 e = (raw[last, [6, 9, 7]] - t0) / 1e3
 print(f"CTA 0 (planner + control block): pass3 done {e[0]:.1f}, epilogue start {e[1]:.1f}, done {e[2]:.1f} us")
-pl = (raw[0, [10, 11]] - t0) / 1e3
-print(f"R update + Givens plan (CTA 0 warp 0, during pass 3): {pl[0]:.1f} -> {pl[1]:.1f} us ({pl[1] - pl[0]:.1f} us)")
+pl = (raw[0, [10, 13, 11]] - t0) / 1e3
+print(f"R update + Givens plan (CTA 0 warp 0, during pass 3): {pl[0]:.1f} -> R assembled {pl[1]:.1f} -> plan done "
+      f"{pl[2]:.1f} us (assembly {pl[1] - pl[0]:.1f} us, plan {pl[2] - pl[1]:.1f} us)")
 
 # ---- k_form_fused of the same (last) step
 L.ig_debug_trace_read_form.argtypes = [C.c_void_p, C.c_int]

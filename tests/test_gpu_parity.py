@@ -367,6 +367,42 @@ def test_c2_full_size_parity():
     he.close()
 
 
+@pytest.mark.slow
+def test_2p24_open_loop_parity():
+    """Open-loop oracle parity at 2^24 DOFs (3D 256^3, HBM-scale: 128 MB vectors, the B~/X~
+    history 2 GB) with QR(8) and EXTRAP(3,8) in the bench launch configuration: every guess vs
+    the oracle, d identical, through history fill and 3 downdates (multi-trip passes and the
+    dynamic pass-3 tail at a size where no vector fits in L2)."""
+    from paper_2009_10863_b200 import InitialGuess
+
+    g = Grid(256, 3)
+    assert g.N == 1 << 24
+    M, steps = 8, 12
+    op, oe = ProjQR(g.N, M), ExtrapLS(g.N, M, 3)
+    hp, he = InitialGuess(g.N, "proj_qr", M), InitialGuess(g.N, "extrap_ls", M, 3)
+    x_prev = np.zeros(g.N)
+    for n in range(steps):
+        b, x, Ax = (t.numpy() for t in manufactured_step(g, n))
+        tb, tx, tA = (torch.from_numpy(v).cuda() for v in (b, x, Ax))
+        x0p = torch.from_numpy(x_prev).cuda()
+        hp.form_guess(tb, x0p)
+        e = _rel(x0p.cpu().numpy(), op.form_guess(b, x_prev))
+        assert e <= TOL, f"step {n}: QR guess {e:.3e}"
+        x0e = torch.from_numpy(x_prev).cuda()
+        he.form_guess(None, x0e)
+        e = _rel(x0e.cpu().numpy(), oe.form_guess(b, x_prev))
+        assert e <= TOL, f"step {n}: EXTRAP guess {e:.3e}"
+        op.update(x, Ax)
+        hp.update(tx, tA)
+        oe.update(x)
+        he.update(tx)
+        assert hp.d == op.d
+        x_prev = x
+        del tb, tx, tA, x0p, x0e
+    hp.close()
+    he.close()
+
+
 # ------------------------------------------------------------------ sparse extrapolation (NEXT row f2)
 @pytest.mark.parametrize("m,M", [(2, 8), (3, 8), (3, 16), (2, 12), (5, 30), (0, 4), (3, 4)])
 def test_sparse_weights_match_exact_cpqr(m, M):
