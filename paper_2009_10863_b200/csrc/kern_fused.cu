@@ -9,9 +9,10 @@
 //
 //   k_form_fused   : [alpha = B~^T b] --barrier--> [x0 = X~ alpha]
 //   k_update_fused : [B~ downdate + c1, ||Ax||^2] --barrier--> [c2, ||b1||^2] --barrier-->
-//                    [X~ downdate + x~, b~, admission, new columns; warp 0 of CTA 0: R update and
-//                    the next downdate's Givens plan, its trips claimed by the others]
-//                    --> CTA 0 writes the control block (no exit barrier)
+//                    [X~ downdate + x~, b~, admission, new columns]
+//                    --> CTA 0 writes the control block (no exit barrier); the planner CTA
+//                    (the last one, QR) computes R and the next downdate's Givens plan
+//                    alongside (its prefix during passes 1-2, its suffix after barrier 2)
 // Barrier and claim counters are double-buffered by a launch epoch in the control block.  The
 // element arithmetic is the same device code as the one-kernel-per-pass path (proj_common.cuh),
 // which stays in use when partial sums cross ranks through an all-gather (ig_attach_comm); with
@@ -145,6 +146,83 @@ __global__ void __launch_bounds__(THREADS, 1) k_form_fused(ProjArgs a) {
     TRACE_F(7);
 }
 
+// Admission of the update's pair (thread 0; AMB-3 / AMB-6 / AMB-8): ||b~2||^2 = ||b~1||^2 - ||c2||^2
+// (B~ orthonormal), relative test; a non-finite sum never admits (the history stays unchanged).
+__device__ __forceinline__ void admission(const double *r1, const double *r2, int deff, double eps, double &nb,
+                                          double &nAx, int &adm) {
+    const double nAx2 = r1[NORM];
+    double nb2;
+    if (deff > 0) {
+        double c2sq = 0.0;
+        for (int k = 0; k < deff; ++k) c2sq = fma(r2[k], r2[k], c2sq);
+        nb2 = r2[NORM] - c2sq;
+    } else {
+        nb2 = nAx2;  // d = 0: b~ = Ax
+    }
+    nb = sqrt(fmax(nb2, 0.0));
+    nAx = sqrt(nAx2);
+    const bool fin = isfinite(nAx2) && (deff == 0 || isfinite(nb2));
+    adm = fin && ((deff > 0) ? (nb > eps * nAx) : (nAx > 0.0));
+}
+
+// The update's serial work -- R after this update and the Givens plan of the next downdate
+// (Alg. 2) -- runs in a dedicated PLANNER CTA (the last CTA of a QR grid), which streams
+// nothing.  At its start it stages the R the plan will act on (the downdated R if this update
+// downdates, else R) in shared memory and, if this update can end with d = M, runs the plan's
+// prefix (rotations 0..M-3, independent of this update's sums: proj_common.cuh) while the
+// streaming CTAs run passes 1 and 2; after barrier 2 it reduces the same block partials in the
+// same order as every other CTA (bitwise-identical sums and decisions), adds the new R column and
+// runs the plan's suffix (one column, one rotation).  The serial chain (L2-latency-bound R assembly
+// ~12 us and ~0.4 us per rotation at M = 30) is off the critical path at every N.  It arrives once
+// at the barrier counter at its start (so CTA 0 advances the launch epoch only after every CTA,
+// planner included, has read it) and never waits at a barrier: barrier p of the streaming CTAs
+// waits for p * ns + 1 arrivals.
+template <int MC>
+__device__ __forceinline__ void planner_cta(const ProjArgs &a, Ctrl *c, unsigned e, unsigned ns, int d, bool pend,
+                                         int deff, unsigned long long ep1, unsigned long long ep2, double *sR,
+                                         double *sW, double *s_r1, double *s_r2, double *pgc, double *pgs) {
+    __shared__ double s_nb, s_nAx;
+    __shared__ int s_adm;
+    const int M = a.M;
+    __syncthreads();  // every thread has read the control block (kernel start)
+    if (threadIdx.x == 0) {
+        __threadfence();
+        atomicAdd(&c->bar[e & 1], 1u);
+    }
+    TRACE(10);
+    const double *Rsrc = pend ? c->Rdn : c->R;  // the R this update starts from (after its downdate)
+    for (int idx = threadIdx.x; idx < MAXM * MAXM; idx += blockDim.x) sR[idx] = Rsrc[idx];
+    __syncthreads();
+    const bool could_plan = deff == M - 1;  // admitted -> d = M -> the next update downdates
+    if (could_plan && threadIdx.x < 32) plan_prefix(M, sR, sW, pgc, pgs, c->Rdn);
+    TRACE(14);
+    grid_wait(&c->bar[e & 1], 2 * ns + 1, &c->err, a.watchdog_ns);  // the streaming CTAs' pass 2 partials
+    TRACE(13);
+    reduce_all_blocks<MC>(deff, true, a.blk, s_r1, (int)ns);
+    if (a.xc.G > 1) peer_allreduce(a.xc, ST_U1, deff, true, s_r1, ep1, &c->err, a.watchdog_ns);
+    if (deff > 0) reduce_all_blocks<MC>(deff, true, a.blk + BLK2, s_r2, (int)ns);
+    if (deff > 0 && a.xc.G > 1) peer_allreduce(a.xc, ST_U2, deff, true, s_r2, ep2, &c->err, a.watchdog_ns);
+    if (threadIdx.x == 0) {
+        double nb, nAx;
+        int adm;
+        admission(s_r1, s_r2, deff, a.eps, nb, nAx, adm);
+        s_nb = nb;
+        s_nAx = nAx;
+        s_adm = adm;
+    }
+    __syncthreads();
+    const bool adm = s_adm != 0;
+    const int dnew = deff + (adm ? 1 : 0);
+    if (threadIdx.x < 32) {
+        r_update(c, M, deff, pend, adm, s_r1, s_r2, s_nb, sR);
+        if (dnew == M) {  // the next update downdates
+            plan_suffix(M, sR, sW, pgc, pgs, c->Rdn);
+            plan_publish(c, M, pgc, pgs);
+        }
+    }
+    TRACE(11);
+}
+
 template <int MC, int VEC>
 __global__ void __launch_bounds__(THREADS, 1) k_update_fused(ProjArgs a) {
     typedef typename VT<VEC>::T V;
@@ -173,6 +251,14 @@ __global__ void __launch_bounds__(THREADS, 1) k_update_fused(ProjArgs a) {
     const bool restart = (a.method == M_PROJ_CLASSIC) && (d >= M);  // Alg. 1 restart
     const int deff = pend ? M - 1 : (restart ? 0 : d);
     const unsigned long long ep1 = c->xepoch[ST_U1] + 1, ep2 = c->xepoch[ST_U2] + 1;
+    // QR grids of >= 2 CTAs: the last CTA is the planner, the others stream (ns of them)
+    const bool has_planner = a.method == M_PROJ_QR && gridDim.x >= 2;
+    const unsigned ns = gridDim.x - (has_planner ? 1u : 0u);
+    const unsigned bt = has_planner ? 1u : 0u;  // the planner's single arrival
+    if (has_planner && blockIdx.x == ns) {
+        planner_cta<MC>(a, c, e, ns, d, pend, deff, ep1, ep2, s_R, s_W, s_r1, s_r2, s_c1, s_c2);
+        return;
+    }
     const L2Pol pol = make_l2pol();
     TRACE(0);
     if (threadIdx.x < MAXM) {
@@ -195,7 +281,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_update_fused(ProjArgs a) {
     const CP c1 = SMC ? (CP)s_c1 : (CP)c1r;
     const CP c2 = SMC ? (CP)s_c2 : (CP)c2r;
     const int64_t nv = a.N / VEC;
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    const int64_t stride = (int64_t)ns * blockDim.x;
     const int64_t i_first = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const bool tail = VEC == 2 && (a.N & 1) && blockIdx.x == 0 && threadIdx.x == 0;
     // ---- pass 1: [Givens rotation of B~] + c1 = B~^T Ax, ||Ax||^2
@@ -214,10 +300,10 @@ __global__ void __launch_bounds__(THREADS, 1) k_update_fused(ProjArgs a) {
     if (deff > 0 && ntrip2 > 0) u2trip_load(pre2, a, i_first + (ntrip2 - 1) * UB * stride, stride, nv, deff, pol.keep);
     block_partials_store<MC + 1>(v, deff, true, a.blk, sh);
     TRACE(1);
-    grid_barrier(&c->bar[e & 1], 1, &c->err, a.watchdog_ns);
+    grid_barrier(&c->bar[e & 1], 1, &c->err, a.watchdog_ns, ns + bt);
     advance_epoch(c, e);
     TRACE(2);
-    reduce_all_blocks<MC>(deff, true, a.blk, s_r1);
+    reduce_all_blocks<MC>(deff, true, a.blk, s_r1, (int)ns);
     TRACE(3);
     if (a.xc.G > 1) peer_allreduce(a.xc, ST_U1, deff, true, s_r1, ep1, &c->err, a.watchdog_ns);
     if (threadIdx.x < MAXM) s_c1[threadIdx.x] = (threadIdx.x < deff) ? s_r1[threadIdx.x] : 0.0;
@@ -240,33 +326,22 @@ __global__ void __launch_bounds__(THREADS, 1) k_update_fused(ProjArgs a) {
             u2trip_compute(r, c1, v);
         }
     }
-    // first trip of pass 3, in flight across barrier 2 -- except in warp 0 of CTA 0, which may
-    // become the Givens planner (see pass 3) and then hands all its trips to the dynamic claims
-    const bool w0 = blockIdx.x == 0 && threadIdx.x < 32;
+    // first trip of pass 3, in flight across barrier 2
     U3Trip<MC, U3, V> pre3;
-    if (!w0) u3trip_load(pre3, a, i_first, stride, nv, deff, pend, true, pol.stream);
+    u3trip_load(pre3, a, i_first, stride, nv, deff, pend, true, pol.stream);
     if (deff > 0) block_partials_store<MC + 1>(v, deff, true, a.blk + BLK2, sh);
     TRACE(4);
-    grid_barrier(&c->bar[e & 1], 2, &c->err, a.watchdog_ns);
+    grid_barrier(&c->bar[e & 1], 2, &c->err, a.watchdog_ns, 2 * ns + bt);
     TRACE(5);
-    if (deff > 0) reduce_all_blocks<MC>(deff, true, a.blk + BLK2, s_r2);
+    if (deff > 0) reduce_all_blocks<MC>(deff, true, a.blk + BLK2, s_r2, (int)ns);
     if (deff > 0 && a.xc.G > 1) peer_allreduce(a.xc, ST_U2, deff, true, s_r2, ep2, &c->err, a.watchdog_ns);
     if (threadIdx.x == 0) {
-        const double nAx2 = s_r1[NORM];
-        double nb2;
-        if (deff > 0) {
-            double c2sq = 0.0;
-            for (int k = 0; k < deff; ++k) c2sq = fma(s_r2[k], s_r2[k], c2sq);
-            nb2 = s_r2[NORM] - c2sq;  // ||b~2||^2 = ||b~1||^2 - ||c2||^2 (B~ orthonormal)
-        } else {
-            nb2 = nAx2;  // d = 0: b~ = Ax
-        }
-        const double nb = sqrt(fmax(nb2, 0.0)), nAx = sqrt(nAx2);
+        double nb, nAx;
+        int adm;
+        admission(s_r1, s_r2, deff, a.eps, nb, nAx, adm);
         s_nb = nb;
         s_nAx = nAx;
-        // AMB-3 / AMB-6; a non-finite sum never admits (the history stays unchanged)
-        const bool fin = isfinite(nAx2) && (deff == 0 || isfinite(nb2));
-        s_adm = fin && ((deff > 0) ? (nb > a.eps * nAx) : (nAx > 0.0));
+        s_adm = adm;
     }
     __syncthreads();
     const bool adm = s_adm != 0;
@@ -280,7 +355,6 @@ __global__ void __launch_bounds__(THREADS, 1) k_update_fused(ProjArgs a) {
     // a zero A x is skipped (AMB-6); for CLASSIC at d >= M that includes the restart:
     // the full history is kept (Alg. 1's restart branch divides by ||b~||)
     const int dnew = (restart && !adm) ? d : deff + (adm ? 1 : 0);
-    const bool newcol = a.method == M_PROJ_QR && adm;  // R_{1:d,d+1} = c1 + c2, R_{d+1,d+1} = ||b~||
     const bool plan = a.method == M_PROJ_QR && dnew == M;  // the next update downdates
     // ---- pass 3: [Givens rotation of X~] + store the admitted pair
     if (adm || pend) {
@@ -290,47 +364,26 @@ __global__ void __launch_bounds__(THREADS, 1) k_update_fused(ProjArgs a) {
         const int64_t chunk = (int64_t)U3 * stride;
         const int64_t trips = (nv + chunk - 1) / chunk;
         const int64_t Ts = trips < 4 ? trips : trips - (trips + 7) / 8;
-        // R after this update and the next downdate's Givens plan need only c1, c2, ||b~|| and the
-        // admission.  One warp (warp 0 of CTA 0, the "planner") computes them here instead of in
-        // the serial epilogue: it runs the plan (serial, cold in the instruction cache: ~5 us at
-        // M = 8, ~35 us at M = 30) right after barrier 2 and leaves all its static trips
-        // ("holes") to the dynamic claims, so the plan overlaps the whole pass.
-        const bool planner = w0 && (pend || newcol);  // warp-uniform
-        const int64_t nh = (pend || newcol) ? Ts : 0;  // the planner's trips 0..Ts-1
-        if (planner) {
-            TRACE(10);
-            r_update(c, M, deff, pend, newcol, s_r1, s_r2, s_nb, s_R);
-            TRACE(13);
-            if (plan) givens_plan(c, M, s_R, s_W);
-            TRACE(11);
-        } else {
-            if (Ts > 0) {
-                if (w0) u3trip_load(pre3, a, i_first, stride, nv, deff, pend, adm, pol.stream);
-                u3trip_store(pre3, a, i_first, stride, nv, deff, pend, adm, inv, c1, c2, gc, gs, pol.stream);
-            }
-            for (int64_t t = 1; t < Ts; ++t) {
-                const int64_t i0 = i_first + t * chunk;
-                U3Trip<MC, U3, V> r;
-                u3trip_load(r, a, i0, stride, nv, deff, pend, adm, pol.stream);
-                u3trip_store(r, a, i0, stride, nv, deff, pend, adm, inv, c1, c2, gc, gs, pol.stream);
-            }
+        if (Ts > 0) u3trip_store(pre3, a, i_first, stride, nv, deff, pend, adm, inv, c1, c2, gc, gs, pol.stream);
+        for (int64_t t = 1; t < Ts; ++t) {
+            const int64_t i0 = i_first + t * chunk;
+            U3Trip<MC, U3, V> r;
+            u3trip_load(r, a, i0, stride, nv, deff, pend, adm, pol.stream);
+            u3trip_store(r, a, i0, stride, nv, deff, pend, adm, inv, c1, c2, gc, gs, pol.stream);
         }
-        // dynamic claims: q < nq -> the tail rows [S, nv) in 32*U3-row chunks; nq <= q < nq + nh ->
-        // the planner's static trip t = q - nq (rows t*chunk + lane + u*stride)
+        // dynamic claims: the tail rows [S, nv) in 32*U3-row chunks
         const int64_t S = Ts * chunk, WCH = 32 * U3;
         const int64_t nq = nv > S ? (nv - S + WCH - 1) / WCH : 0;
-        if (nq + nh > 0) {
+        if (nq > 0) {
             const int lane = threadIdx.x & 31;
             unsigned q = (lane == 0) ? atomicAdd(&c->dyn3[e & 1], 1u) : 0u;
             q = __shfl_sync(0xffffffffu, q, 0);
-            while ((int64_t)q < nq + nh) {
+            while ((int64_t)q < nq) {
                 unsigned qn = (lane == 0) ? atomicAdd(&c->dyn3[e & 1], 1u) : 0u;  // claim the next one early
                 U3Trip<MC, U3, V> r;
-                const bool tchunk = (int64_t)q < nq;  // one copy of the trip code for both kinds
-                const int64_t i0 = tchunk ? S + (int64_t)q * WCH + lane : ((int64_t)q - nq) * chunk + lane;
-                const int64_t st = tchunk ? 32 : stride;
-                u3trip_load(r, a, i0, st, nv, deff, pend, adm, pol.stream);
-                u3trip_store(r, a, i0, st, nv, deff, pend, adm, inv, c1, c2, gc, gs, pol.stream);
+                const int64_t i0 = S + (int64_t)q * WCH + lane;
+                u3trip_load(r, a, i0, 32, nv, deff, pend, adm, pol.stream);
+                u3trip_store(r, a, i0, 32, nv, deff, pend, adm, inv, c1, c2, gc, gs, pol.stream);
                 q = __shfl_sync(0xffffffffu, qn, 0);
             }
         }
@@ -350,6 +403,15 @@ __global__ void __launch_bounds__(THREADS, 1) k_update_fused(ProjArgs a) {
         return;
     }
     TRACE(9);
+    if (!has_planner && a.method == M_PROJ_QR && threadIdx.x < 32) {
+        // single-CTA grid: R update and plan here, serially (CTA 0 read c->gc at its start)
+        const bool newcol = adm;
+        const double *Rsrc = pend ? c->Rdn : c->R;
+        for (int idx = threadIdx.x; idx < MAXM * MAXM; idx += 32) s_R[idx] = Rsrc[idx];
+        __syncwarp();
+        r_update(c, M, deff, pend, newcol, s_r1, s_r2, s_nb, s_R);
+        if (plan) givens_plan(c, M, s_R, s_W, s_c1, s_c2);  // s_c1/s_c2 are free after pass 3
+    }
     if (threadIdx.x < PS) {
         a.part[ST_U1 * PS + threadIdx.x] = s_r1[threadIdx.x];
         a.part[ST_U2 * PS + threadIdx.x] = (deff > 0) ? s_r2[threadIdx.x] : 0.0;

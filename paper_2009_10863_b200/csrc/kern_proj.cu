@@ -292,7 +292,8 @@ __global__ void __launch_bounds__(THREADS, 1) k_u3(ProjArgs a) {
         c->rotX = 0;
         c->ticket[ST_U3] = 0;
     }
-    if (a.method == M_PROJ_QR && dnew == M && threadIdx.x < 32) givens_plan(c, M, c->R, s_W);
+    // (s_gc / s_gs are free: this block finished its pass-3 trips)
+    if (a.method == M_PROJ_QR && dnew == M && threadIdx.x < 32) givens_plan(c, M, c->R, s_W, s_gc, s_gs);
 }
 
 // ------------------------------------------------------------------ launchers

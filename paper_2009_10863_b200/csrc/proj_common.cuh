@@ -172,13 +172,13 @@ __device__ __forceinline__ bool block_partials_ticket(double (&v)[NV], int nc, b
 // in order (shared memory).  Few registers, so the trip prefetched across a barrier stays resident
 // even at M = 32.  Deterministic for a given grid.  Every thread of the block must call it.
 template <int MC>
-__device__ __forceinline__ void final_reduce(int nc, bool norm, const double *blk, double *out) {
+__device__ __forceinline__ void final_reduce(int nc, bool norm, const double *blk, double *out, int nblk = -1) {
     constexpr int NS = MC + 1;
     constexpr int TPS = THREADS / NS;
     constexpr int CHK = NS > 17 ? 24 : 12;
     __shared__ double s_part[NS * TPS];
     const int t = threadIdx.x, q = t / TPS, r = t % TPS;
-    const int nb = gridDim.x;
+    const int nb = nblk > 0 ? nblk : (int)gridDim.x;  // blocks that stored partials
     if (q < NS) {
         const bool act = (q < MC) ? (q < nc) : norm;
         double acc = 0.0;
@@ -227,12 +227,29 @@ __device__ __forceinline__ unsigned long long globaltimer_ns() {
 // the host reports IG_E_STATE at the next synchronising call (ig_get_stats / ig_history_dim).
 __device__ __forceinline__ void watchdog_trip(int *err, int code) { atomicCAS(err, 0, code); }
 
-__device__ __forceinline__ void grid_barrier(unsigned *ctr, unsigned phase, int *err, unsigned long long limit) {
+// The wait ends at `target` arrivals (default phase * gridDim.x; k_update_fused's planner CTA
+// arrives once at its start and never waits at a barrier, see there).
+__device__ __forceinline__ void grid_wait(unsigned *ctr, unsigned target, int *err, unsigned long long limit) {
+    if (threadIdx.x == 0) {
+        const unsigned long long t0 = globaltimer_ns();
+        while (ld_acquire_u32(ctr) < target) {
+            __nanosleep(20);
+            if (globaltimer_ns() - t0 > limit) {
+                watchdog_trip(err, 1);
+                break;
+            }
+        }
+        __threadfence();
+    }
+    __syncthreads();
+}
+__device__ __forceinline__ void grid_barrier(unsigned *ctr, unsigned phase, int *err, unsigned long long limit,
+                                             unsigned target = 0) {
     __syncthreads();
     if (threadIdx.x == 0) {
         __threadfence();
         atomicAdd(ctr, 1u);
-        const unsigned target = phase * gridDim.x;
+        if (target == 0) target = phase * gridDim.x;
         const unsigned long long t0 = globaltimer_ns();
         while (ld_acquire_u32(ctr) < target) {
             __nanosleep(20);
@@ -265,8 +282,8 @@ __device__ __forceinline__ void advance_epoch(Ctrl *c, unsigned e) {
 // Every CTA reduces all block partials of a stage in the same fixed order (so all CTAs hold
 // bitwise-identical sums) into out[slot] (shared memory).  Ends with __syncthreads().
 template <int MC>
-__device__ __forceinline__ void reduce_all_blocks(int nc, bool norm, const double *blk, double *out) {
-    final_reduce<MC>(nc, norm, blk, out);
+__device__ __forceinline__ void reduce_all_blocks(int nc, bool norm, const double *blk, double *out, int nblk = -1) {
+    final_reduce<MC>(nc, norm, blk, out, nblk);
     __syncthreads();
 }
 
@@ -635,60 +652,106 @@ __device__ __forceinline__ void u3trip_store(const U3Trip<MC, U, V> &r, const Pr
     }
 }
 
-// One warp: Givens parameters of the next downdate from R (AMB-2 reading of P:279-290):
-// H = R_{:,2:M}; for i: a = H_ii, b = H_{i+1,i}, r = hypot(a,b), c = a/r, s = b/r; rotate rows.
-// Lane j owns column j of H (W[i*32 + j], shared scratch); `t` is its entry in the row carried
-// down (row i after rotations < i), b = H_{i+1,i} = R_{i+1,i+1}: one shuffle per rotation.  Row i
-// is final after rotation i and goes straight to Rdn.  Only the leading M x M block of R / Rdn
-// is touched.  The loops stay rolled on purpose: this runs once per call in a serial tail where
-// the code is cold in the instruction cache (an unrolled version measured 13 us cold vs 2.7 us
-// warm at M = 8), so code size, not instruction count, sets its time.
-static __device__ __noinline__ void givens_plan(Ctrl *c, int M, const double *R, double *W) {
+// Givens plan of the next downdate (AMB-2 reading of P:279-290): H = R_{:,2:M} (upper
+// Hessenberg, H_ij = R_{i,j+1}); rotation i = 0..M-2 takes a = H_ii (after rotations < i),
+// b = H_{i+1,i} = R_{i+1,i+1}, r = hypot(a, b), c = a/r, s = b/r and rotates rows (i, i+1) of H;
+// row i of the downdated R is final after rotation i.  One warp; lane j owns H column j (its
+// entry of the row carried down in `t`, the rows below in W[i*32 + j], shared).
+// Rotation i reads only H columns <= i, i.e. R columns <= i+1, so rotations 0..M-3 need R columns
+// 0..M-2 only -- which an update does not change: the column it may add (R column M-1 = H column
+// M-2) enters the last rotation alone.  The plan is therefore split:
+//   plan_prefix: rotations 0..M-3 on H columns 0..M-3 (lanes j <= M-3): Rdn columns 0..M-3 and
+//                (c_i, s_i), i <= M-3 -- computable before the update's sums are known;
+//   plan_suffix: H column M-2 through rotations 0..M-3, then rotation M-2 (Rdn column M-2, the zero
+//                fill of the leading block, (c, s) of M-2).
+// R: the R the downdate acts on (leading M x M block, column-major, stride MAXM; shared or global);
+// Rdn: global; pgc/pgs: shared; W: shared [MAXM*32].  Explicit fma() pins the rounding, so the
+// split and the one-piece plan (givens_plan) give bitwise-identical results.  The loops stay rolled:
+// this code runs once per call, cold in the instruction cache.
+static __device__ __noinline__ void plan_prefix(int M, const double *R, double *W, double *pgc, double *pgs,
+                                                double *Rdn) {
     const int j = threadIdx.x & 31;
 #pragma unroll 1
-    for (int i = 0; i < M; ++i) W[i * 32 + j] = (j < M - 1) ? R[i + (j + 1) * MAXM] : 0.0;  // H_ij = R_{i,j+1}
+    for (int i = 0; i < M; ++i) W[i * 32 + j] = (j < M - 2) ? R[i + (j + 1) * MAXM] : 0.0;  // H_ij, j <= M-3
     __syncwarp();
-    double t = W[j], my_c = 1.0, my_s = 0.0;
+    double t = W[j];
 #pragma unroll 1
-    for (int i = 0; i < M - 1; ++i) {
+    for (int i = 0; i < M - 2; ++i) {
         const double aa = __shfl_sync(0xffffffffu, t, i);
         const double bb = R[(i + 1) + (i + 1) * MAXM];
         const double r = hypot(aa, bb);
         const double cs = (r == 0.0) ? 1.0 : aa / r;
         const double sn = (r == 0.0) ? 0.0 : bb / r;
         if (j == i) {
-            my_c = cs;
-            my_s = sn;
+            pgc[i] = cs;
+            pgs[i] = sn;
         }
-        if (j >= i && j < M - 1) {
+        if (j >= i && j < M - 2) {
             const double hi1 = W[(i + 1) * 32 + j];
-            c->Rdn[i + j * MAXM] = cs * t + sn * hi1;
-            t = -sn * t + cs * hi1;
+            Rdn[i + j * MAXM] = fma(cs, t, sn * hi1);
+            t = fma(cs, hi1, -(sn * t));
+        }
+    }
+    __syncwarp();
+}
+static __device__ __noinline__ void plan_suffix(int M, const double *R, double *W, double *pgc, double *pgs,
+                                                double *Rdn) {
+    const int j = threadIdx.x & 31;
+    if (M >= 2) {
+        if (j < M) W[j * 32 + (M - 2)] = R[j + (M - 1) * MAXM];  // H column M-2 = R column M-1
+        __syncwarp();
+        if (j == M - 2) {
+            double t = W[M - 2];
+#pragma unroll 1
+            for (int i = 0; i < M - 2; ++i) {
+                const double cs = pgc[i], sn = pgs[i], hi1 = W[(i + 1) * 32 + j];
+                Rdn[i + j * MAXM] = fma(cs, t, sn * hi1);
+                t = fma(cs, hi1, -(sn * t));
+            }
+            const int i = M - 2;
+            const double bb = R[(i + 1) + (i + 1) * MAXM];
+            const double r = hypot(t, bb);
+            const double cs = (r == 0.0) ? 1.0 : t / r;
+            const double sn = (r == 0.0) ? 0.0 : bb / r;
+            pgc[i] = cs;
+            pgs[i] = sn;
+            Rdn[i + j * MAXM] = fma(cs, t, sn * W[(i + 1) * 32 + j]);
         }
     }
     if (j < M)  // the rest of the leading block of the downdated R is zero
 #pragma unroll 1
         for (int i = 0; i < M; ++i)
-            if (!(i < M - 1 && j < M - 1 && i <= j)) c->Rdn[i + j * MAXM] = 0.0;
+            if (!(i < M - 1 && j < M - 1 && i <= j)) Rdn[i + j * MAXM] = 0.0;
+    __syncwarp();
+}
+// Publish the plan: (c_i, s_i) for the next update's B~/X~ rotations, pending downdate.
+static __device__ __forceinline__ void plan_publish(Ctrl *c, int M, const double *pgc, const double *pgs) {
+    const int j = threadIdx.x & 31;
     if (j < M - 1) {
-        c->gc[j] = my_c;
-        c->gs[j] = my_s;
+        c->gc[j] = pgc[j];
+        c->gs[j] = pgs[j];
     }
     __syncwarp();
     if (j == 0) c->pending = 1;
 }
+// One-piece plan (split schedule, single-CTA grids): prefix + suffix + publish.
+static __device__ __noinline__ void givens_plan(Ctrl *c, int M, const double *R, double *W, double *pgc,
+                                                double *pgs) {
+    plan_prefix(M, R, W, pgc, pgs, c->Rdn);
+    plan_suffix(M, R, W, pgc, pgs, c->Rdn);
+    plan_publish(c, M, pgc, pgs);
+}
 
-// One warp: R after this update -- its leading M x M block is the downdated R (if a downdate ran)
-// plus, if the pair was admitted, the new column (c1 + c2; ||b~||) (Alg. 2) -- stored
-// to c->R and to sR (shared); the caller then runs givens_plan from sR if the next update downdates.
+// One warp: R after this update, in place in sR (which holds the R it started from: the downdated
+// R if a downdate ran, else R) -- plus, if the pair was admitted, the new column (c1 + c2; ||b~||)
+// (Alg. 2) -- and to c->R.
 static __device__ __noinline__ void r_update(Ctrl *c, int M, int deff, bool pend, bool newcol, const double *r1,
                                              const double *r2, double nb, double *sR) {
     const int lane = threadIdx.x & 31;
-    const double *Rsrc = pend ? c->Rdn : c->R;
 #pragma unroll 1
     for (int idx = lane; idx < M * M; idx += 32) {
         const int i = idx % M, j = idx / M;
-        double v = Rsrc[i + j * MAXM];
+        double v = sR[i + j * MAXM];
         if (newcol && j == deff) v = (i < deff) ? r1[i] + r2[i] : (i == deff ? nb : 0.0);
         sR[i + j * MAXM] = v;
         if (pend || (newcol && j == deff)) c->R[i + j * MAXM] = v;

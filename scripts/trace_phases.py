@@ -27,7 +27,9 @@ L = lib()
 L.ig_debug_trace_read.argtypes = [C.c_void_p, C.c_int]
 buf = (C.c_ulonglong * (1024 * 16))()
 assert L.ig_debug_trace_read(buf, 1024 * 16) == 0
-raw = np.array(buf[:148 * 16], dtype=np.float64).reshape(148, 16)
+allrows = np.array(buf[:148 * 16], dtype=np.float64).reshape(148, 16)
+plan_row = allrows[147]  # QR grids: the last CTA is the planner (streams nothing)
+raw = allrows[:147]
 t = raw[:, [8, 0, 1, 2, 3, 4, 5, 6, 7]]
 last = 0  # CTA 0 writes the control block (no exit barrier)
 t0 = t[:, 0].min()
@@ -38,9 +40,9 @@ for j, nm in enumerate(names):
     print(f"{nm:14s} min {t[:, j].min():8.1f} med {np.median(t[:, j]):8.1f} max {t[:, j].max():8.1f} us")
 e = (raw[last, [6, 9, 7]] - t0) / 1e3
 print(f"CTA 0 (planner + control block): pass3 done {e[0]:.1f}, epilogue start {e[1]:.1f}, done {e[2]:.1f} us")
-pl = (raw[0, [10, 13, 11]] - t0) / 1e3
-print(f"R update + Givens plan (CTA 0 warp 0, during pass 3): {pl[0]:.1f} -> R assembled {pl[1]:.1f} -> plan done "
-      f"{pl[2]:.1f} us (assembly {pl[1] - pl[0]:.1f} us, plan {pl[2] - pl[1]:.1f} us)")
+pl = (plan_row[[8, 10, 14, 13, 11]] - t0) / 1e3
+print(f"planner CTA: begin {pl[0]:.1f}, staged R {pl[1]:.1f}, plan prefix done {pl[2]:.1f}, saw barrier 2 {pl[3]:.1f}, "
+      f"R + plan suffix done {pl[4]:.1f} us (after barrier 2: {pl[4] - pl[3]:.1f} us)")
 
 # ---- k_form_fused of the same (last) step
 L.ig_debug_trace_read_form.argtypes = [C.c_void_p, C.c_int]
@@ -56,7 +58,7 @@ sm_u = raw[:, 12].astype(int)
 sm_f = rf[:, 12].astype(int)
 du = {s: (raw[i, 1] - raw[i, 0]) / 1e3 for i, s in enumerate(sm_u)}
 df = {s: (rf[i, 1] - rf[i, 0]) / 1e3 for i, s in enumerate(sm_f)}
-common = sorted(set(du) & set(df))
+common = sorted((set(du) & set(df)) - {int(plan_row[12])})
 a = np.array([du[s] for s in common]); b = np.array([df[s] for s in common])
 print(f"pass-1 duration per SM: update {a.mean():.1f}+-{a.std():.2f} us, form {b.mean():.1f}+-{b.std():.2f} us, "
       f"corr over {len(common)} SMs = {np.corrcoef(a, b)[0, 1]:.2f}")
