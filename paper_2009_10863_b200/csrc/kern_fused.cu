@@ -252,11 +252,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_update_fused(ProjArgs a) {
     const int deff = pend ? M - 1 : (restart ? 0 : d);
     const unsigned long long ep1 = c->xepoch[ST_U1] + 1, ep2 = c->xepoch[ST_U2] + 1;
     // QR grids of >= 2 CTAs: the last CTA is the planner, the others stream (ns of them)
-#ifdef IG_NO_PLANNER  // experiment builds only: plan serially in CTA 0's epilogue
-    const bool has_planner = false;
-#else
     const bool has_planner = a.method == M_PROJ_QR && gridDim.x >= 2;
-#endif
     const unsigned ns = gridDim.x - (has_planner ? 1u : 0u);
     const unsigned bt = has_planner ? 1u : 0u;  // the planner's single arrival
     if (has_planner && blockIdx.x == ns) {
@@ -367,10 +363,8 @@ __global__ void __launch_bounds__(THREADS, 1) k_update_fused(ProjArgs a) {
         // CTAs on slower SMs take fewer tail chunks, so all CTAs reach the exit together.
         const int64_t chunk = (int64_t)U3 * stride;
         const int64_t trips = (nv + chunk - 1) / chunk;
-#ifndef IG_TAIL_DIV
-#define IG_TAIL_DIV 8
-#endif
-        const int64_t Ts = trips < 4 ? trips : trips - (trips + IG_TAIL_DIV - 1) / IG_TAIL_DIV;
+        // (1/4 and 1/16 of the rows measured no better: profiles/r2_planner_ab.md)
+        const int64_t Ts = trips < 4 ? trips : trips - (trips + 7) / 8;
         if (Ts > 0) u3trip_store(pre3, a, i_first, stride, nv, deff, pend, adm, inv, c1, c2, gc, gs, pol.stream);
         for (int64_t t = 1; t < Ts; ++t) {
             const int64_t i0 = i_first + t * chunk;
@@ -388,14 +382,8 @@ __global__ void __launch_bounds__(THREADS, 1) k_update_fused(ProjArgs a) {
             while ((int64_t)q < nq) {
                 unsigned qn = (lane == 0) ? atomicAdd(&c->dyn3[e & 1], 1u) : 0u;  // claim the next one early
                 U3Trip<MC, U3, V> r;
-#ifdef IG_EXP_CLAIM  // experiment: the round-1 claim-loop form (variable stride)
-                const bool tchunk = (int64_t)q < nq;
-                const int64_t i0 = tchunk ? S + (int64_t)q * WCH + lane : ((int64_t)q - nq) * chunk + lane;
-                const int64_t st = tchunk ? 32 : stride;
-#else
                 const int64_t i0 = S + (int64_t)q * WCH + lane;
                 const int64_t st = 32;
-#endif
                 u3trip_load(r, a, i0, st, nv, deff, pend, adm, pol.stream);
                 u3trip_store(r, a, i0, st, nv, deff, pend, adm, inv, c1, c2, gc, gs, pol.stream);
                 q = __shfl_sync(0xffffffffu, qn, 0);
