@@ -47,7 +47,7 @@ namespace ig {
 constexpr int BLK2 = PS * MAXB;
 
 template <int MC, int VEC>
-__global__ void __launch_bounds__(THREADS, 1) k_form_fused(ProjArgs a) {
+__global__ void __launch_bounds__(THREADS, 1) k_form_fused(const __grid_constant__ ProjArgs a) {
     typedef typename VT<VEC>::T V;
     constexpr int U = FusedUnroll<MC>::U;
     __shared__ double sh[(THREADS / 32) * (MC + 1)];
@@ -178,13 +178,21 @@ __device__ __forceinline__ void admission(const double *r1, const double *r2, in
 // planner included, has read it) and never waits at a barrier: barrier p of the streaming CTAs
 // waits for p * ns + 1 arrivals.
 template <int MC>
-__device__ __forceinline__ void planner_cta(const ProjArgs &a, Ctrl *c, unsigned e, unsigned ns, int d, bool pend,
-                                         int deff, unsigned long long ep1, unsigned long long ep2, double *sR,
-                                         double *sW, double *s_r1, double *s_r2, double *pgc, double *pgs) {
+__device__ __noinline__ void planner_cta(const ProjArgs &a, unsigned ns) {
+    // its own shared arrays and control-block reads: a small call interface keeps the streaming
+    // CTAs' register allocation independent of this code, which is also laid out away from the
+    // streaming passes (their cold code per launch is fetched from L2 under full HBM load)
+    __shared__ double sR[MAXM * MAXM], sW[MAXM * 32], s_r1[PS], s_r2[PS], pgc[MAXM], pgs[MAXM];
     __shared__ double s_nb, s_nAx;
     __shared__ int s_adm;
+    Ctrl *c = a.ctrl;
     const int M = a.M;
-    __syncthreads();  // every thread has read the control block (kernel start)
+    const unsigned e = *(volatile unsigned *)&c->epoch;
+    const int d = c->d;
+    const bool pend = c->pending != 0;
+    const int deff = pend ? M - 1 : d;
+    const unsigned long long ep1 = c->xepoch[ST_U1] + 1, ep2 = c->xepoch[ST_U2] + 1;
+    __syncthreads();  // every thread has read the control block
     if (threadIdx.x == 0) {
         __threadfence();
         atomicAdd(&c->bar[e & 1], 1u);
@@ -224,7 +232,7 @@ __device__ __forceinline__ void planner_cta(const ProjArgs &a, Ctrl *c, unsigned
 }
 
 template <int MC, int VEC>
-__global__ void __launch_bounds__(THREADS, 1) k_update_fused(ProjArgs a) {
+__global__ void __launch_bounds__(THREADS, 1) k_update_fused(const __grid_constant__ ProjArgs a) {
     typedef typename VT<VEC>::T V;
     constexpr int U = FusedUnroll<MC>::U;
     __shared__ double sh[(THREADS / 32) * (MC + 1)];
@@ -256,7 +264,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_update_fused(ProjArgs a) {
     const unsigned ns = gridDim.x - (has_planner ? 1u : 0u);
     const unsigned bt = has_planner ? 1u : 0u;  // the planner's single arrival
     if (has_planner && blockIdx.x == ns) {
-        planner_cta<MC>(a, c, e, ns, d, pend, deff, ep1, ep2, s_R, s_W, s_r1, s_r2, s_c1, s_c2);
+        planner_cta<MC>(a, ns);
         return;
     }
     const L2Pol pol = make_l2pol();
