@@ -623,3 +623,37 @@ def test_properties_at_full_size(N, M, p):
     assert np.max(np.abs(got - ref)) <= 1e-13 * np.max(np.abs(ref)) * np.abs(beta).sum()
     ig.close()
     ie.close()
+
+
+# ------------------------------------------------------------------ planner CTA edge grids
+@pytest.mark.parametrize("grid", [1, 2, 3, 37])
+@pytest.mark.parametrize("M", [1, 2, 8, 30])
+def test_planner_cta_and_single_cta_grids(grid, M):
+    """The last CTA of a QR update grid is the planner (R update + Givens plan); with a
+    one-CTA grid the plan runs serially in CTA 0.  Grids of 1, 2 (one streaming CTA + planner),
+    3 and 37 CTAs through fill and downdates: every guess matches the oracle, d identical, and the
+    history equals the full-grid run's to rounding."""
+    from paper_2009_10863_b200 import InitialGuess, ig_set_grid_limit
+
+    g = Grid(37, 2)  # N = 1369: ragged, several trips per thread on small grids
+    seq = _seq(g, 2 * M + 4, dt=1e-2)
+    ora = ProjQR(g.N, M)
+    ig = InitialGuess(g.N, "proj_qr", M)
+    ig_set_grid_limit(ig.h, grid)
+    ref = InitialGuess(g.N, "proj_qr", M)
+    x_prev = np.zeros(g.N)
+    for n, (b, x, Ax) in enumerate(seq):
+        x0 = torch.from_numpy(x_prev).cuda()
+        x0r = x0.clone()
+        ig.form_guess(torch.from_numpy(b).cuda(), x0)
+        ref.form_guess(torch.from_numpy(b).cuda(), x0r)
+        e = _rel(x0.cpu().numpy(), ora.form_guess(b, x_prev))
+        assert e <= TOL, f"grid {grid} step {n}: {e:.3e}"
+        assert _rel(x0.cpu().numpy(), x0r.cpu().numpy()) <= TOL
+        ora.update(x, Ax)
+        ig.update(torch.from_numpy(x).cuda(), torch.from_numpy(Ax).cuda())
+        ref.update(torch.from_numpy(x).cuda(), torch.from_numpy(Ax).cuda())
+        assert ig.d == ora.d
+        x_prev = x
+    ig.close()
+    ref.close()
