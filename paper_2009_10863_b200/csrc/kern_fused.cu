@@ -373,28 +373,67 @@ __global__ void __launch_bounds__(THREADS, 1) k_update_fused(const __grid_consta
         const int64_t trips = (nv + chunk - 1) / chunk;
         // (1/4 and 1/16 of the rows measured no better: profiles/r2_planner_ab.md)
         const int64_t Ts = trips < 4 ? trips : trips - (trips + 7) / 8;
-        if (Ts > 0) u3trip_store(pre3, a, i_first, stride, nv, deff, pend, adm, inv, c1, c2, gc, gs, pol.stream);
-        for (int64_t t = 1; t < Ts; ++t) {
-            const int64_t i0 = i_first + t * chunk;
-            U3Trip<MC, U3, V> r;
-            u3trip_load(r, a, i0, stride, nv, deff, pend, adm, pol.stream);
-            u3trip_store(r, a, i0, stride, nv, deff, pend, adm, inv, c1, c2, gc, gs, pol.stream);
-        }
         // dynamic claims: the tail rows [S, nv) in 32*U3-row chunks
-        const int64_t S = Ts * chunk, WCH = 32 * U3;
-        const int64_t nq = nv > S ? (nv - S + WCH - 1) / WCH : 0;
-        if (nq > 0) {
+        // M <= 32 bucket below 2^24 DOFs: ONE copy of the ~1900-instruction trip code serves the
+        // static trips and the claims, loading at the end of each iteration for the next item --
+        // the pass's hot code is half the size, which pays once it no longer fits the instruction
+        // cache and the pass is short (profiles/r2_onecopy_ab.md: N = 1e6 QR(17) 255 -> 230,
+        // QR(30) 357 -> 339 us); at 2^27 the two-copy form below is as fast or faster, so large
+        // vectors keep it (a uniform branch per launch).  The M <= 16 bucket keeps two copies: any
+        // change there moved its register allocation into a 5-19 % slower pass 1 at large N.
+        bool one_copy = false;
+        if constexpr (MC >= 32) one_copy = a.N < (int64_t(1) << 24);
+        if (one_copy) {
+            const int64_t S = Ts * chunk, WCH = 32 * U3;
+            const int64_t nq = nv > S ? (nv - S + WCH - 1) / WCH : 0;
             const int lane = threadIdx.x & 31;
-            unsigned q = (lane == 0) ? atomicAdd(&c->dyn3[e & 1], 1u) : 0u;
-            q = __shfl_sync(0xffffffffu, q, 0);
-            while ((int64_t)q < nq) {
-                unsigned qn = (lane == 0) ? atomicAdd(&c->dyn3[e & 1], 1u) : 0u;  // claim the next one early
+            // ONE copy of the (large: ~1900 instructions at M = 32) trip code for the static trips
+            // and the claims, loads at the end of each iteration for the next item: the pass's hot
+            // code is half the size, which matters once it no longer fits the instruction cache
+            if (Ts > 0) {
+                int64_t t = 0, i0 = i_first, st = stride;
+                unsigned qn = 0xffffffffu;
+                while (true) {
+                    if (nq > 0 && t >= Ts - 1) {  // the next item is a claim: take its ticket now
+                        unsigned v = (lane == 0) ? atomicAdd(&c->dyn3[e & 1], 1u) : 0u;
+                        qn = __shfl_sync(0xffffffffu, v, 0);
+                    }
+                    u3trip_store(pre3, a, i0, st, nv, deff, pend, adm, inv, c1, c2, gc, gs, pol.stream);
+                    if (t + 1 < Ts) {
+                        ++t;
+                        i0 = i_first + t * chunk;
+                        st = stride;
+                    } else {
+                        t = Ts;
+                        if ((int64_t)qn >= nq) break;  // also nq == 0 (qn stays ~0)
+                        i0 = S + (int64_t)qn * WCH + lane;
+                        st = 32;
+                    }
+                    u3trip_load(pre3, a, i0, st, nv, deff, pend, adm, pol.stream);
+                }
+            }
+        } else {
+            if (Ts > 0) u3trip_store(pre3, a, i_first, stride, nv, deff, pend, adm, inv, c1, c2, gc, gs, pol.stream);
+            for (int64_t t = 1; t < Ts; ++t) {
+                const int64_t i0 = i_first + t * chunk;
                 U3Trip<MC, U3, V> r;
-                const int64_t i0 = S + (int64_t)q * WCH + lane;
-                const int64_t st = 32;
-                u3trip_load(r, a, i0, st, nv, deff, pend, adm, pol.stream);
-                u3trip_store(r, a, i0, st, nv, deff, pend, adm, inv, c1, c2, gc, gs, pol.stream);
-                q = __shfl_sync(0xffffffffu, qn, 0);
+                u3trip_load(r, a, i0, stride, nv, deff, pend, adm, pol.stream);
+                u3trip_store(r, a, i0, stride, nv, deff, pend, adm, inv, c1, c2, gc, gs, pol.stream);
+            }
+            const int64_t S = Ts * chunk, WCH = 32 * U3;
+            const int64_t nq = nv > S ? (nv - S + WCH - 1) / WCH : 0;
+            if (nq > 0) {
+                const int lane = threadIdx.x & 31;
+                unsigned q = (lane == 0) ? atomicAdd(&c->dyn3[e & 1], 1u) : 0u;
+                q = __shfl_sync(0xffffffffu, q, 0);
+                while ((int64_t)q < nq) {
+                    unsigned qn = (lane == 0) ? atomicAdd(&c->dyn3[e & 1], 1u) : 0u;  // claim the next one early
+                    U3Trip<MC, U3, V> r;
+                    const int64_t i0 = S + (int64_t)q * WCH + lane;
+                    u3trip_load(r, a, i0, 32, nv, deff, pend, adm, pol.stream);
+                    u3trip_store(r, a, i0, 32, nv, deff, pend, adm, inv, c1, c2, gc, gs, pol.stream);
+                    q = __shfl_sync(0xffffffffu, qn, 0);
+                }
             }
         }
         if (tail) {

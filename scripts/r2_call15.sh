@@ -2,7 +2,7 @@
 # A/B: one-copy pass-3 trip loop for the M <= 32 bucket (cur) vs 5f8e36f
 mkdir -p gpurun_out
 python -c "from paper_2009_10863_b200.build import build; build()" > gpurun_out/build.log 2>&1
-timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_api_sequences.py -q -x -k "30 or 32 or 17 or random or sequence" -p no:cacheprovider 2>&1 | tail -2
+timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_api_sequences.py -q -x -p no:cacheprovider 2>&1 | tail -2
 for rep in 1 2; do for wt in 5f8e36f cur; do
   if [ $wt = cur ]; then D=.; else D=build/wt_$wt; fi
   echo "== $wt"; (cd $D && timeout 900 python scripts/bench_sweep.py --sizes 100000,1000000,10000000,134217728 --ms 17,24,30 --steps 20 2>&1 | grep '^{' | python /root/repo/scripts/probes/sweep_short.py)
