@@ -207,7 +207,11 @@ int ig_set_device_ring(ig_t h, int on);
  *   ig_graph_launch(g, stream): one replay (asynchronous on `stream`).
  *   ig_graph_destroy(g): releases it (NULL: no-op).
  * The captured calls bind the device pointers passed at capture time: each step the caller
- * writes its new b / x / Ax into those buffers (or solves into them) before the replay.
+ * writes its new b / x / Ax into those buffers (or solves into them) before the replay.  A graph
+ * refers to its handles' history storage: destroy it before the handles.  Calls that synchronise
+ * (ig_history_dim, ig_get_stats, ig_bytes, ig_next_slot of a device window, the *_host variants,
+ * checkpoint calls, ig_set_device_ring) must not be issued while capturing (IG_E_STATE or a
+ * CUDA capture error).  Begin and end a capture on the same host thread.
  * ig_total_launches() counts the captured libig kernels once per replay, not at capture. */
 typedef struct ig_graph_ctx *ig_graph_t;
 int ig_capture_begin(void *cuda_stream);

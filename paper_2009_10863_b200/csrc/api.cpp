@@ -407,6 +407,8 @@ void ring_set_host(ig_t h, unsigned long long cnt) {
 // Host mirror of a device window (syncs the stream): for the introspection / checkpoint calls.
 int ring_pull(ig_t h) {
     if (!h->dring) return IG_OK;
+    if (capturing(h->stream))  // a synchronising read would invalidate the caller's capture
+        return set_err(IG_E_STATE, "the device window position cannot be read while the stream is being captured");
     DevRing r;
     CUDA_OK(cudaMemcpyAsync(&r, h->ring, sizeof r, cudaMemcpyDeviceToHost, h->stream));
     CUDA_OK(cudaStreamSynchronize(h->stream));
@@ -415,6 +417,8 @@ int ring_pull(ig_t h) {
 }
 int ring_push_host(ig_t h) {  // host window -> device counter (enqueued; syncs: r is a stack object)
     if (!h->dring) return IG_OK;
+    if (capturing(h->stream))
+        return set_err(IG_E_STATE, "the device window cannot be (re)positioned while the stream is being captured");
     DevRing r = {ring_cnt_of(h), 0u, 0u};
     CUDA_OK(cudaMemcpyAsync(h->ring, &r, sizeof r, cudaMemcpyHostToDevice, h->stream));
     CUDA_OK(cudaStreamSynchronize(h->stream));

@@ -189,3 +189,33 @@ def test_captured_multi_field_step_matches_the_oracle(n_side):
     step.close()
     for h in igs:
         h.close()
+
+
+def test_sync_calls_refused_during_capture():
+    """A synchronising read of a device window during capture would invalidate the caller's
+    capture: it is refused (IG_E_STATE) and the capture stays usable."""
+    from paper_2009_10863_b200 import IGError, InitialGuess, ig_capture_begin, ig_capture_end, ig_graph_destroy
+    from paper_2009_10863_b200 import ig_graph_launch
+
+    N = 2000
+    s = torch.cuda.Stream()
+    h = InitialGuess(N, "extrap_ls", 4, 2, stream=s)
+    h.set_device_ring(True)
+    x = torch.ones(N, dtype=torch.float64, device="cuda")
+    x0 = torch.zeros(N, dtype=torch.float64, device="cuda")
+    torch.cuda.synchronize()
+    ig_capture_begin(s)
+    with pytest.raises(IGError):
+        _ = h.d
+    with pytest.raises(IGError):
+        h.set_device_ring(False)
+    h.form_guess(None, x0)
+    h.update(x)
+    g = ig_capture_end(s)
+    for _ in range(3):
+        ig_graph_launch(g, s)
+    s.synchronize()
+    assert h.d == 3
+    assert torch.equal(x0, torch.ones(N, dtype=torch.float64, device="cuda"))  # 2 pushes of ones -> guess 1
+    ig_graph_destroy(g)
+    h.close()
