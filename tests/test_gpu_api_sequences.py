@@ -3,7 +3,9 @@ restart, fill/head of the window, launch epochs and barrier counters of the pers
 must give the oracle's guess after ANY sequence of the public calls -- forms without updates,
 updates without forms, zero right-hand sides (skip / rejection), repeated pairs (rejection),
 resets, checkpoint -> restore into a fresh handle, switching between the fused and the split
-schedule, device- and host-buffer entry points.  Every guess within 1e-11 of the oracle
+schedule, host / device extrapolation windows (ig_set_device_ring), persistent-kernel grids of
+1, 2, 7 CTAs or the full GPU (the planner CTA and its single-CTA fallback), device- and
+host-buffer entry points.  Every guess within 1e-11 of the oracle
 (PAPER.md:253-308 for QR / CLASSIC, Eq. EXTRAPEXPN for EXTRAP)."""
 
 import os
@@ -41,7 +43,8 @@ _EXTRA = int(os.environ.get("IG_SEQ_SEEDS", "0"))  # soak: IG_SEQ_SEEDS=50 adds 
 def test_random_call_sequences_match_oracle(seed, n):
     """n = 27: one grid-stride trip per thread; n = 600 (360,000 DOFs): several trips, so the
     dynamically claimed pass-3 tail and the Givens planner's handed-off trips are exercised."""
-    from paper_2009_10863_b200 import (InitialGuess, ig_form_guess_host, ig_set_schedule, ig_update_host)
+    from paper_2009_10863_b200 import (InitialGuess, ig_form_guess_host, ig_set_grid_limit, ig_set_schedule,
+                                       ig_update_host)
 
     rng = np.random.default_rng(seed)
     g = Grid(n, 2)
@@ -53,7 +56,7 @@ def test_random_call_sequences_match_oracle(seed, n):
     from paper_2009_10863_b200 import ig_form_guess_batch, ig_update_batch
 
     ops = ["form", "form", "update", "update", "update", "update_zero", "update_repeat", "reset", "save_load",
-           "schedule", "form_host", "update_host", "update_inplace", "form_batch", "update_batch"]
+           "schedule", "form_host", "update_host", "update_inplace", "form_batch", "update_batch", "ring", "grid"]
     last = [None] * len(SPECS)
     checked = 0
     for step in range(70):
@@ -124,6 +127,10 @@ def test_random_call_sequences_match_oracle(seed, n):
         elif op == "schedule" and method != "extrap_ls":
             fused[i] = not fused[i]
             ig_set_schedule(h.h, fused[i])
+        elif op == "ring" and method == "extrap_ls":  # host <-> device window, history kept
+            h.set_device_ring(bool(rng.integers(2)))
+        elif op == "grid" and method != "extrap_ls":  # 1 CTA, planner + 1 or 6 streaming CTAs, full GPU
+            ig_set_grid_limit(h.h, int(rng.choice([0, 1, 2, 7])))
         if method != "extrap_ls":
             assert h.d == o.d, (seed, step, op, method)
     assert checked >= 10

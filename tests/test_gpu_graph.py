@@ -219,3 +219,81 @@ def test_sync_calls_refused_during_capture():
     assert torch.equal(x0, torch.ones(N, dtype=torch.float64, device="cuda"))  # 2 pushes of ones -> guess 1
     ig_graph_destroy(g)
     h.close()
+
+
+@pytest.mark.parametrize("seed", [11, 12, 13])
+def test_replays_interleaved_with_eager_calls(seed):
+    """A captured step (guess + update of a QR field and two extrapolation fields) replayed at
+    random points of a sequence that also makes eager calls, resets and window-mode switches on
+    the same handles: the graph reads and advances the same device state, so every guess matches
+    the oracle's at every point."""
+    from paper_2009_10863_b200 import CapturedStep, InitialGuess, ig_form_guess_batch, ig_update_batch
+
+    rng = np.random.default_rng(seed)
+    g = Grid(40, 2)
+    N = g.N
+    specs = [("proj_qr", 6, 0), ("extrap_ls", 6, 2), ("extrap_sparse", 8, 2)]
+    mk = {"proj_qr": lambda M, p: ProjQR(N, M), "extrap_ls": lambda M, p: ExtrapLS(N, M, p),
+          "extrap_sparse": lambda M, p: ExtrapSparse(N, M, p)}
+    oras = [mk[m](M, p) for m, M, p in specs]
+    s = torch.cuda.Stream()
+    hs = [InitialGuess(N, m, M, p, stream=s) for m, M, p in specs]
+    for h in hs[1:]:
+        h.set_device_ring(True)
+    F = len(specs)
+    seq = _seq(g, 30, dt=1e-2)
+    bufs = {k: [torch.zeros(N, dtype=torch.float64, device="cuda") for _ in range(F)] for k in ("b", "x0", "x", "Ax")}
+    torch.cuda.synchronize()
+    with CapturedStep(s) as step:
+        ig_form_guess_batch(hs, bufs["b"], bufs["x0"])
+        ig_update_batch(hs, bufs["x"], bufs["Ax"])
+
+    def check(got, f, ref, tag):
+        nr = np.linalg.norm(ref)
+        assert np.linalg.norm(got - ref) <= TOL * (nr if nr > 0 else 1.0), (seed, tag, specs[f])
+
+    for it in range(40):
+        b, x, Ax = seq[int(rng.integers(len(seq)))]
+        op = rng.choice(["replay", "replay", "eager", "reset", "switch"])
+        if op == "replay":
+            # the graph was captured with device windows: make sure they are on
+            for h in hs[1:]:
+                h.set_device_ring(True)
+            with torch.cuda.stream(s):
+                for f in range(F):
+                    bufs["b"][f].copy_(torch.from_numpy(b))
+                    bufs["x0"][f].zero_()
+                    bufs["x"][f].copy_(torch.from_numpy(x))
+                    bufs["Ax"][f].copy_(torch.from_numpy(Ax))
+            step.replay()
+            s.synchronize()
+            for f, o in enumerate(oras):
+                check(bufs["x0"][f].cpu().numpy(), f, o.form_guess(b, np.zeros(N)), ("replay", it))
+                o.update(x, Ax)
+        elif op == "eager":
+            f = int(rng.integers(F))
+            x0 = torch.zeros(N, dtype=torch.float64, device="cuda")
+            with torch.cuda.stream(s):
+                hs[f].form_guess(torch.from_numpy(b).cuda(), x0)
+                hs[f].update(torch.from_numpy(x).cuda(), torch.from_numpy(Ax).cuda())
+            s.synchronize()
+            check(x0.cpu().numpy(), f, oras[f].form_guess(b, np.zeros(N)), ("eager", it))
+            oras[f].update(x, Ax)
+        elif op == "reset":
+            f = int(rng.integers(F))
+            hs[f].reset()
+            m, M, p = specs[f]
+            oras[f] = mk[m](M, p)
+        else:  # switch an extrapolation field's window to the host and back (history kept)
+            f = 1 + int(rng.integers(F - 1))
+            hs[f].set_device_ring(False)
+            x0 = torch.zeros(N, dtype=torch.float64, device="cuda")
+            with torch.cuda.stream(s):
+                hs[f].form_guess(None, x0)
+            s.synchronize()
+            check(x0.cpu().numpy(), f, oras[f].form_guess(None, np.zeros(N)), ("host window", it))
+        for f, (h, o) in enumerate(zip(hs, oras)):
+            assert h.d == (o.d if hasattr(o, "d") else o.fill), (seed, it, specs[f])
+    step.close()
+    for h in hs:
+        h.close()
