@@ -231,7 +231,9 @@ __device__ __noinline__ void planner_cta(const ProjArgs &a, unsigned ns) {
     TRACE(11);
 }
 
-template <int MC, int VEC>
+// OC: the one-copy pass-3 loop (see pass 3); a separate instantiation, chosen by the launcher for the
+// M > 8 buckets below 2^24 DOFs, so the large-vector kernels keep their exact code and registers.
+template <int MC, int VEC, bool OC = false>
 __global__ void __launch_bounds__(THREADS, 1) k_update_fused(const __grid_constant__ ProjArgs a) {
     typedef typename VT<VEC>::T V;
     constexpr int U = FusedUnroll<MC>::U;
@@ -374,16 +376,13 @@ __global__ void __launch_bounds__(THREADS, 1) k_update_fused(const __grid_consta
         // (1/4 and 1/16 of the rows measured no better: profiles/r2_planner_ab.md)
         const int64_t Ts = trips < 4 ? trips : trips - (trips + 7) / 8;
         // dynamic claims: the tail rows [S, nv) in 32*U3-row chunks
-        // M <= 32 bucket below 2^24 DOFs: ONE copy of the ~1900-instruction trip code serves the
-        // static trips and the claims, loading at the end of each iteration for the next item --
-        // the pass's hot code is half the size, which pays once it no longer fits the instruction
-        // cache and the pass is short (profiles/r2_onecopy_ab.md: N = 1e6 QR(17) 255 -> 230,
-        // QR(30) 357 -> 339 us); at 2^27 the two-copy form below is as fast or faster, so large
-        // vectors keep it (a uniform branch per launch).  The M <= 16 bucket keeps two copies: any
-        // change there moved its register allocation into a 5-19 % slower pass 1 at large N.
-        bool one_copy = false;
-        if constexpr (MC >= 32) one_copy = a.N < (int64_t(1) << 24);
-        if (one_copy) {
+        // OC (M > 8 buckets below 2^24 DOFs): ONE copy of the large trip code (~900 / ~1900
+        // instructions at M = 16 / 32) serves the static trips and the claims, loading at the end of
+        // each iteration for the next item -- the pass's hot code is half the size, which pays once
+        // it no longer fits the instruction cache and the pass is short (profiles/r2_onecopy_ab.md:
+        // N = 1e6 QR(12) 145.6 -> 138.1, QR(17) 255 -> 230, QR(30) 357 -> 339 us); at 2^27 the
+        // two-copy form is as fast or faster, so large vectors use the OC = false kernel.
+        if constexpr (OC) {
             const int64_t S = Ts * chunk, WCH = 32 * U3;
             const int64_t nq = nv > S ? (nv - S + WCH - 1) / WCH : 0;
             const int lane = threadIdx.x & 31;
@@ -527,6 +526,10 @@ cudaError_t launch_form_fused(const ProjArgs &a, int vec, int nsm, cudaStream_t 
     IG_FUSED_DISPATCH(k_form_fused, a, vec, nsm, s);
 }
 cudaError_t launch_update_fused(const ProjArgs &a, int vec, int nsm, cudaStream_t s) {
+    const int mc = mcb(a.M);
+    if (vec == 2 && mc >= 16 && a.N < (int64_t(1) << 24))
+        return mc == 16 ? coop_launch(k_update_fused<16, 2, true>, a, nsm, s)
+                        : coop_launch(k_update_fused<32, 2, true>, a, nsm, s);
     IG_FUSED_DISPATCH(k_update_fused, a, vec, nsm, s);
 }
 
