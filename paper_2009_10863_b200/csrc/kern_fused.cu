@@ -46,6 +46,14 @@ namespace ig {
 // partials a slow CTA is still reading.
 constexpr int BLK2 = PS * MAXB;
 
+// Smallest bucket whose one-copy (OC) update kernel uses the rolling prefetch in passes 1 and 2
+// (u1_roll / u2_roll; bitwise-identical results; A/B on one box, profiles/r3_roll_ab.md: N = 3e5
+// QR(16) 49.5 -> 48.0, 1e6 QR(12) 137.0 -> 134.0, QR(24) 281.2 -> 275.3, QR(30) 339 -> 336,
+// 3e6 QR(16) 510 -> 505, 1e7 QR(16) 1615 -> 1601 us/step).  -DIG_ROLL_MIN=64 turns it off.
+#ifndef IG_ROLL_MIN
+#define IG_ROLL_MIN 16
+#endif
+
 template <int MC, int VEC>
 __global__ void __launch_bounds__(THREADS, 1) k_form_fused(const __grid_constant__ ProjArgs a) {
     typedef typename VT<VEC>::T V;
@@ -299,7 +307,22 @@ __global__ void __launch_bounds__(THREADS, 1) k_update_fused(const __grid_consta
 #pragma unroll
     for (int k = 0; k <= MC; ++k) v[k] = 0.0;
     constexpr int UU1 = U;  // pass-1 elements per trip
-    for (int64_t i0 = i_first; i0 < nv; i0 += UU1 * stride) u1_trip<MC, UU1, V>(a, i0, stride, nv, pend, deff, gc, gs, v, pol.keep);
+    // ROLL: rolling prefetch in passes 1 and 2 (one element per trip; u1_roll / u2_roll)
+    constexpr bool ROLL = OC && MC >= IG_ROLL_MIN && U == 1 && FusedUnroll<MC>::U2 == 1;
+    if constexpr (ROLL) {
+        U2Trip<MC, 1, V> r1;
+        const int nload = pend ? M : deff;
+        if (i_first < nv) u2trip_load(r1, a, i_first, stride, nv, nload, pol.keep);
+        if (pend) {
+            for (int64_t i = i_first; i < nv; i += stride)
+                u1_roll<MC, true>(r1, a, i, i + stride, i + stride < nv, nload, gc, gs, v, pol.keep);
+        } else {
+            for (int64_t i = i_first; i < nv; i += stride)
+                u1_roll<MC, false>(r1, a, i, i + stride, i + stride < nv, nload, gc, gs, v, pol.keep);
+        }
+    } else {
+        for (int64_t i0 = i_first; i0 < nv; i0 += UU1 * stride) u1_trip<MC, UU1, V>(a, i0, stride, nv, pend, deff, gc, gs, v, pol.keep);
+    }
     if (tail) u1_trip<MC, 1, double>(a, a.N - 1, 1, a.N, pend, deff, gc, gs, v, pol.keep);
     // Serpentine order: pass 2 walks the vectors BACKWARDS, so it starts on the B~/Ax lines pass 1
     // touched last (still in the 126 MB L2); pass 3 walks forwards again and starts on what pass 2
@@ -326,9 +349,13 @@ __global__ void __launch_bounds__(THREADS, 1) k_update_fused(const __grid_consta
     if (deff > 0) {
 #pragma unroll
         for (int k = 0; k <= MC; ++k) v[k] = 0.0;
-        for (int64_t t = ntrip2 - 1; t >= 0; --t) {  // one copy of the trip code (pre2 = the first)
-            if (t < ntrip2 - 1) u2trip_load(pre2, a, i_first + t * UB * stride, stride, nv, deff, pol.keep);
-            u2trip_compute(pre2, c1, v);
+        if constexpr (ROLL) {
+            for (int64_t t = ntrip2 - 1; t >= 0; --t) u2_roll(pre2, a, i_first + (t - 1) * stride, t > 0, deff, c1, v, pol.keep);
+        } else {
+            for (int64_t t = ntrip2 - 1; t >= 0; --t) {  // one copy of the trip code (pre2 = the first)
+                if (t < ntrip2 - 1) u2trip_load(pre2, a, i_first + t * UB * stride, stride, nv, deff, pol.keep);
+                u2trip_compute(pre2, c1, v);
+            }
         }
         if (tail) {
             U2Trip<MC, 1, double> r;

@@ -571,6 +571,64 @@ __device__ __forceinline__ void u2trip_compute(const U2Trip<MC, U, V> &r, CP c1,
     }
 }
 
+// Rolling prefetch for the one-element-per-trip passes 1 and 2 of the large buckets (RollTrip =
+// the U2Trip<MC, 1, V> layout: Ax and the B~ columns of one element): the next trip's load of a
+// column is issued as soon as this trip has consumed that column, so about one trip of 16-byte
+// loads stays in flight per thread through the arithmetic -- the loads of a warp no longer come
+// in bursts separated by its compute, and the SM's bytes in flight stop depending on whether its
+// eight warps happen to run in phase.  Same rows, same per-thread accumulation order as
+// u1_trip / u2trip_compute (bitwise-identical sums).
+// Column addresses of the next element advance by one running pointer (one add per column): with
+// 32 columns, base + k*ld per column made ptxas keep 32 hoisted 64-bit column pointers live.
+template <int MC, bool pend, class V, class CP>
+__device__ __forceinline__ void u1_roll(U2Trip<MC, 1, V> &r, const ProjArgs &a, int64_t i, int64_t inext, bool okn,
+                                        int nload, CP gc, CP gs, double (&v)[MC + 1], unsigned long long pk) {
+    const V ax = r.ax[0];
+    r.ax[0] = okn ? ldp<V>(a.Ax, inext, pk) : vzero(V());
+    v[MC] = vdot(ax, ax, v[MC]);
+    const double *pn = a.Bt + inext * (int64_t)(sizeof(V) / sizeof(double));  // column 0, next element
+    double *ps = a.Bt + i * (int64_t)(sizeof(V) / sizeof(double));            // column 0, this element
+    if constexpr (pend) {
+        V t = r.col[0][0];
+        r.col[0][0] = (okn && 0 < nload) ? ldp<V>(pn, 0, pk) : vzero(V());
+#pragma unroll
+        for (int k = 0; k < MC - 1; ++k) {
+            if (k < a.M - 1) {
+                V nk;
+                pn += a.ld;
+                vrot(gc[k], gs[k], t, r.col[0][k + 1], nk);
+                r.col[0][k + 1] = (okn && k + 1 < nload) ? ldp<V>(pn, 0, pk) : vzero(V());
+                stp<V>(ps, 0, nk, pk);
+                ps += a.ld;
+                v[k] = vdot(nk, ax, v[k]);
+            }
+        }
+    } else {
+#pragma unroll
+        for (int k = 0; k < MC; ++k) {
+            v[k] = vdot(r.col[0][k], ax, v[k]);
+            r.col[0][k] = (okn && k < nload) ? ldp<V>(pn, 0, pk) : vzero(V());
+            pn += a.ld;
+        }
+    }
+}
+template <int MC, class V, class CP>
+__device__ __forceinline__ void u2_roll(U2Trip<MC, 1, V> &r, const ProjArgs &a, int64_t inext, bool okn, int deff,
+                                        CP c1, double (&v)[MC + 1], unsigned long long pk) {
+    V b1 = r.ax[0];  // b1 = Ax - B~ c1 (registers only)
+    r.ax[0] = okn ? ldp<V>(a.Ax, inext, pk) : vzero(V());
+#pragma unroll
+    for (int k = 0; k < MC; ++k) b1 = vaxpy(-c1[k], r.col[0][k], b1);
+    const double *pn = a.Bt + inext * (int64_t)(sizeof(V) / sizeof(double));
+#pragma unroll
+    for (int k = 0; k < MC; ++k) {
+        v[k] = vdot(r.col[0][k], b1, v[k]);
+        r.col[0][k] = (okn && k < deff) ? ldp<V>(pn, 0, pk) : vzero(V());
+        pn += a.ld;
+    }
+    v[MC] = vdot(b1, b1, v[MC]);
+}
+
 // For MC >= 32 (SPLIT) a trip holds only Ax, x and the B~ columns; the X~ columns are loaded
 // (all at once) after the B~ part is finished, so the two 32-column register sets are never live
 // together and the pass can use 16-byte loads (VEC = 2) within the register file.
