@@ -53,6 +53,13 @@ constexpr int BLK2 = PS * MAXB;
 #ifndef IG_ROLL_MIN
 #define IG_ROLL_MIN 16
 #endif
+// Smallest bucket whose one-copy update kernel runs pass 3 with rolling register sets (u3_roll;
+// buckets whose B~ and X~ columns fit in registers together, i.e. MC = 16; bitwise-identical;
+// profiles/r3_roll_ab.md: N = 1e6 QR(16) 171.9 -> 169.5, QR(12) 133.2 -> 131.8, QR(9) 109.3 ->
+// 108.3 us/step; 1e7 QR(16) 1602 -> 1609).  -DIG_ROLL3_MIN=64 turns it off.
+#ifndef IG_ROLL3_MIN
+#define IG_ROLL3_MIN 16
+#endif
 
 template <int MC, int VEC>
 __global__ void __launch_bounds__(THREADS, 1) k_form_fused(const __grid_constant__ ProjArgs a) {
@@ -363,9 +370,14 @@ __global__ void __launch_bounds__(THREADS, 1) k_update_fused(const __grid_consta
             u2trip_compute(r, c1, v);
         }
     }
-    // first trip of pass 3, in flight across barrier 2
+    // first trip of pass 3, in flight across barrier 2 (ROLL3: the B~ part of the first element)
+    constexpr bool ROLL3 = OC && MC >= IG_ROLL3_MIN && U3 == 1 && !U3Trip<MC, 1, V>::SPLIT;
     U3Trip<MC, U3, V> pre3;
-    u3trip_load(pre3, a, i_first, stride, nv, deff, pend, true, pol.stream);
+    R3<MC, V> r3;
+    if constexpr (ROLL3)
+        r3_load(r3, a, i_first, i_first < nv, deff, pend, true, pol.stream);
+    else
+        u3trip_load(pre3, a, i_first, stride, nv, deff, pend, true, pol.stream);
     if (deff > 0) block_partials_store<MC + 1>(v, deff, true, a.blk + BLK2, sh);
     TRACE(4);
     grid_barrier(&c->bar[e & 1], 2, &c->err, a.watchdog_ns, 2 * ns + bt);
@@ -409,7 +421,29 @@ __global__ void __launch_bounds__(THREADS, 1) k_update_fused(const __grid_consta
         // it no longer fits the instruction cache and the pass is short (profiles/r2_onecopy_ab.md:
         // N = 1e6 QR(12) 145.6 -> 138.1, QR(17) 255 -> 230, QR(30) 357 -> 339 us); at 2^27 the
         // two-copy form is as fast or faster, so large vectors use the OC = false kernel.
-        if constexpr (OC) {
+        if constexpr (ROLL3) {
+            // as the OC loop below, with the rolling register set: the next item (static trip or
+            // claim) is known before the current one is processed
+            const int64_t S = Ts * chunk, WCH = 32;
+            const int64_t nq = nv > S ? (nv - S + WCH - 1) / WCH : 0;
+            const int lane = threadIdx.x & 31;
+            if (Ts > 0) {
+                int64_t t = 0, i0 = i_first;
+                unsigned qn = 0xffffffffu;
+                while (true) {
+                    if (nq > 0 && t >= Ts - 1) {  // the next item is a claim: take its ticket now
+                        unsigned v = (lane == 0) ? atomicAdd(&c->dyn3[e & 1], 1u) : 0u;
+                        qn = __shfl_sync(0xffffffffu, v, 0);
+                    }
+                    const bool has = (t + 1 < Ts) || ((int64_t)qn < nq);  // also nq == 0 (qn stays ~0)
+                    const int64_t in = (t + 1 < Ts) ? i_first + (t + 1) * chunk : S + (int64_t)qn * WCH + lane;
+                    u3_roll(r3, a, i0, i0 < nv, in, has && in < nv, deff, pend, adm, inv, c1, c2, gc, gs, pol.stream);
+                    if (!has) break;
+                    t = (t + 1 < Ts) ? t + 1 : Ts;
+                    i0 = in;
+                }
+            }
+        } else if constexpr (OC) {
             const int64_t S = Ts * chunk, WCH = 32 * U3;
             const int64_t nq = nv > S ? (nv - S + WCH - 1) / WCH : 0;
             const int lane = threadIdx.x & 31;

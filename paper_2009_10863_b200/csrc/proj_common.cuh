@@ -712,6 +712,89 @@ __device__ __forceinline__ void u3trip_store(const U3Trip<MC, U, V> &r, const Pr
     }
 }
 
+// Pass 3 with rolling register sets (one element per trip, the one-copy kernels, buckets whose
+// B~ and X~ columns fit in registers together): slot k of the B~ set is consumed by the two
+// Gram-Schmidt sums of element i and then receives B~ column k of the NEXT element; slot k of
+// the X~ set is consumed by the X~ part (rotation / combine) and receives X~ column k of the next
+// element.  Every load is issued a whole element ahead of its use, so about 2M 16-byte loads per
+// thread stay in flight through the arithmetic (the unrolled form issues them in one burst after
+// the element's stores and then waits).  Same expressions in the same order as u3trip_store
+// (bitwise-identical results).  (A single rolling set -- X~ of element i loaded into the B~
+// slots right after the sums -- waits a full memory latency per element: 1.3-1.4x slower.)
+template <int MC, class V> struct R3 {
+    V ax, xv;
+    V bs[MC], xs[MC];
+};
+template <int MC, class V>
+__device__ __forceinline__ void r3_load(R3<MC, V> &r, const ProjArgs &a, int64_t i, bool ok, int deff, bool rotX,
+                                        bool adm, unsigned long long ps) {
+    const int nB = adm ? deff : 0;
+    const int nX = rotX ? a.M : nB;
+    r.ax = (ok && adm) ? ldp<V>(a.Ax, i, ps) : vzero(V());
+    r.xv = (ok && adm) ? ldp<V>(a.x, i, ps) : vzero(V());
+    const double *pb = a.Bt + i * (int64_t)(sizeof(V) / sizeof(double));
+    const double *px = a.Xt + i * (int64_t)(sizeof(V) / sizeof(double));
+#pragma unroll
+    for (int k = 0; k < MC; ++k) {
+        r.bs[k] = (ok && k < nB) ? ldp<V>(pb, 0, ps) : vzero(V());
+        r.xs[k] = (ok && k < nX) ? ldp<V>(px, 0, ps) : vzero(V());
+        pb += a.ld;
+        px += a.ld;
+    }
+}
+// Element i (valid iff ok) from r; loads element inext (iff okn) into r on the way.
+template <int MC, class V, class CP>
+__device__ __forceinline__ void u3_roll(R3<MC, V> &r, const ProjArgs &a, int64_t i, bool ok, int64_t inext, bool okn,
+                                        int deff, bool rotX, bool adm, double inv, CP c1, CP c2, CP gc, CP gs,
+                                        unsigned long long ps) {
+    constexpr int64_t W = sizeof(V) / sizeof(double);
+    const int nB = adm ? deff : 0;
+    const int nX = rotX ? a.M : nB;
+    // b~ = (Ax - B~ c1) - B~ c2 ; x~ = (x - X~ c1) - X~ c2 (separate corrections, DESIGN.md AMB-7)
+    V b1 = r.ax, s2 = vzero(V());
+    r.ax = (okn && adm) ? ldp<V>(a.Ax, inext, ps) : vzero(V());
+#pragma unroll
+    for (int k = 0; k < MC; ++k) b1 = vaxpy(-c1[k], r.bs[k], b1);
+    const double *pb = a.Bt + inext * W;
+#pragma unroll
+    for (int k = 0; k < MC; ++k) {
+        s2 = vaxpy(c2[k], r.bs[k], s2);
+        r.bs[k] = (okn && k < nB) ? ldp<V>(pb, 0, ps) : vzero(V());
+        pb += a.ld;
+    }
+    if (adm && ok) stp<V>(a.Bt + deff * a.ld, i, vscale(inv, vaxpy(-1.0, s2, b1)), ps);
+    V xt = r.xv, t2 = vzero(V());
+    r.xv = (okn && adm) ? ldp<V>(a.x, inext, ps) : vzero(V());
+    const double *pn = a.Xt + inext * W;
+    if (rotX) {
+        double *pxs = a.Xt + i * W;
+        V t = r.xs[0];
+        r.xs[0] = (okn && 0 < nX) ? ldp<V>(pn, 0, ps) : vzero(V());
+#pragma unroll
+        for (int k = 0; k < MC - 1; ++k) {
+            if (k < a.M - 1) {
+                V nk;
+                pn += a.ld;
+                vrot(gc[k], gs[k], t, r.xs[k + 1], nk);
+                r.xs[k + 1] = (okn && k + 1 < nX) ? ldp<V>(pn, 0, ps) : vzero(V());
+                if (ok) stp<V>(pxs, 0, nk, ps);
+                pxs += a.ld;
+                xt = vaxpy(-c1[k], nk, xt);
+                t2 = vaxpy(c2[k], nk, t2);
+            }
+        }
+    } else {
+#pragma unroll
+        for (int k = 0; k < MC; ++k) {
+            xt = vaxpy(-c1[k], r.xs[k], xt);
+            t2 = vaxpy(c2[k], r.xs[k], t2);
+            r.xs[k] = (okn && k < nX) ? ldp<V>(pn, 0, ps) : vzero(V());
+            pn += a.ld;
+        }
+    }
+    if (adm && ok) stp<V>(a.Xt + deff * a.ld, i, vscale(inv, vaxpy(-1.0, t2, xt)), ps);
+}
+
 // Givens plan of the next downdate (AMB-2 reading of P:279-290): H = R_{:,2:M} (upper
 // Hessenberg, H_ij = R_{i,j+1}); rotation i = 0..M-2 takes a = H_ii (after rotations < i),
 // b = H_{i+1,i} = R_{i+1,i+1}, r = hypot(a, b), c = a/r, s = b/r and rotates rows (i, i+1) of H;
