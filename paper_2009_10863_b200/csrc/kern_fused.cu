@@ -61,7 +61,10 @@ constexpr int BLK2 = PS * MAXB;
 #define IG_ROLL3_MIN 16
 #endif
 
-template <int MC, int VEC>
+// RF: rolling prefetch in both passes (one element per trip, u1_roll-style: the next element's
+// load of a column is issued as soon as this element has consumed it); a separate instantiation
+// chosen by the launcher for the M > 8 buckets below 2^24 DOFs (bitwise-identical results).
+template <int MC, int VEC, bool RF = false>
 __global__ void __launch_bounds__(THREADS, 1) k_form_fused(const __grid_constant__ ProjArgs a) {
     typedef typename VT<VEC>::T V;
     constexpr int U = FusedUnroll<MC>::U;
@@ -93,6 +96,34 @@ __global__ void __launch_bounds__(THREADS, 1) k_form_fused(const __grid_constant
     double v[MC + 1];
 #pragma unroll
     for (int k = 0; k <= MC; ++k) v[k] = 0.0;
+    constexpr int64_t W = VEC;
+    if constexpr (RF) {
+        static_assert(UP == 1 && FusedUnroll<MC>::FORM_P2 == 1 && FusedUnroll<MC>::FORM_PF == 1, "RF: one element per trip");
+        V bv = vzero(V()), col[MC];
+        {
+            const bool ok = i_first < nv;
+            const double *p = a.Bt + i_first * W;
+            if (ok) bv = ldp<V>(a.b, i_first, ps);
+#pragma unroll
+            for (int k = 0; k < MC; ++k) {
+                col[k] = (ok && k < d) ? ldp<V>(p, 0, ps) : vzero(V());
+                p += a.ld;
+            }
+        }
+        for (int64_t i = i_first; i < nv; i += stride) {
+            const int64_t in = i + stride;
+            const bool okn = in < nv;
+            const V bc = bv;
+            bv = okn ? ldp<V>(a.b, in, ps) : vzero(V());
+            const double *p = a.Bt + in * W;
+#pragma unroll
+            for (int k = 0; k < MC; ++k) {
+                v[k] = vdot(col[k], bc, v[k]);
+                col[k] = (okn && k < d) ? ldp<V>(p, 0, ps) : vzero(V());
+                p += a.ld;
+            }
+        }
+    } else
     for (int64_t i0 = i_first; i0 < nv; i0 += UP * stride) {
         V bv[UP], col[UP][MC];
 #pragma unroll
@@ -134,12 +165,29 @@ __global__ void __launch_bounds__(THREADS, 1) k_form_fused(const __grid_constant
 #pragma unroll
     for (int k = 0; k < MC; ++k) al[k] = (k < d) ? s_red[k] : 0.0;
     // ---- pass 2: x0 = X~ alpha (b fully consumed before the barrier: x0 may alias b)
+    if constexpr (RF) {
+        XTrip<MC, UX, V> &r = pre[0];  // element i_first, loaded before the barrier
+        for (int64_t i = i_first; i < nv; i += stride) {
+            const int64_t in = i + stride;
+            const bool okn = in < nv;
+            const double *p = a.Xt + in * W;
+            V acc = vzero(V());
 #pragma unroll
-    for (int f = 0; f < FP; ++f) xtrip_store(pre[f], a, i_first + f * UX * stride, stride, nv, al);
-    for (int64_t i0 = i_first + FP * UX * stride; i0 < nv; i0 += UX * stride) {
-        XTrip<MC, UX, V> r;
-        xtrip_load(r, a, i0, stride, nv, d, ps);
-        xtrip_store(r, a, i0, stride, nv, al);
+            for (int k = 0; k < MC; ++k) {
+                acc = vaxpy(al[k], r.col[0][k], acc);
+                r.col[0][k] = (okn && k < d) ? ldp<V>(p, 0, ps) : vzero(V());
+                p += a.ld;
+            }
+            stv<V>(a.x0, i, acc);
+        }
+    } else {
+#pragma unroll
+        for (int f = 0; f < FP; ++f) xtrip_store(pre[f], a, i_first + f * UX * stride, stride, nv, al);
+        for (int64_t i0 = i_first + FP * UX * stride; i0 < nv; i0 += UX * stride) {
+            XTrip<MC, UX, V> r;
+            xtrip_load(r, a, i0, stride, nv, d, ps);
+            xtrip_store(r, a, i0, stride, nv, al);
+        }
     }
     if (VEC == 2 && (a.N & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
         const int64_t i = a.N - 1;
@@ -583,7 +631,15 @@ static int mcb(int M) { return M <= 1 ? 1 : M <= 2 ? 2 : M <= 4 ? 4 : M <= 8 ? 8
         }                                                                                           \
     } while (0)
 
+// Rolling form kernel for M = 17..32 below 2^24 DOFs (A/B, profiles/r3_roll_ab.md: N = 1e6
+// QR(30) 335.5 -> 330.8, 1e7 QR(30) 3024 -> 2987 us/step; neutral at M = 16 and 0.8 us slower at
+// 3e5 QR(12), so the M <= 16 buckets keep the unrolled form).  -DIG_FORM_RF=0 turns it off.
+#ifndef IG_FORM_RF
+#define IG_FORM_RF 1
+#endif
 cudaError_t launch_form_fused(const ProjArgs &a, int vec, int nsm, cudaStream_t s) {
+    if (IG_FORM_RF && vec == 2 && mcb(a.M) == 32 && a.N < (int64_t(1) << 24))
+        return coop_launch(k_form_fused<32, 2, true>, a, nsm, s);
     IG_FUSED_DISPATCH(k_form_fused, a, vec, nsm, s);
 }
 cudaError_t launch_update_fused(const ProjArgs &a, int vec, int nsm, cudaStream_t s) {
