@@ -53,6 +53,13 @@ constexpr int BLK2 = PS * MAXB;
 #ifndef IG_ROLL_MIN
 #define IG_ROLL_MIN 16
 #endif
+// The same for the large-vector (two-copy) kernels: the M = 17..32 bucket only (the M = 16
+// kernel's register allocation is fragile); profiles/r3_roll_ab.md, with the rolling
+// form kernel: N = 2e7 QR(17) 3956 -> 3710, QR(30) 5988 -> 5896; 2^27 QR(24) 33564 -> 32948,
+// QR(30) 40394 -> 39937 us/step.
+#ifndef IG_ROLL_BIG_MIN
+#define IG_ROLL_BIG_MIN 32
+#endif
 // Smallest bucket whose one-copy update kernel runs pass 3 with rolling register sets (u3_roll;
 // buckets whose B~ and X~ columns fit in registers together, i.e. MC = 16; bitwise-identical;
 // profiles/r3_roll_ab.md: N = 1e6 QR(16) 171.9 -> 169.5, QR(12) 133.2 -> 131.8, QR(9) 109.3 ->
@@ -63,7 +70,7 @@ constexpr int BLK2 = PS * MAXB;
 
 // RF: rolling prefetch in both passes (one element per trip, u1_roll-style: the next element's
 // load of a column is issued as soon as this element has consumed it); a separate instantiation
-// chosen by the launcher for the M > 8 buckets below 2^24 DOFs (bitwise-identical results).
+// chosen by the launcher for the M = 17..32 bucket (bitwise-identical results).
 template <int MC, int VEC, bool RF = false>
 __global__ void __launch_bounds__(THREADS, 1) k_form_fused(const __grid_constant__ ProjArgs a) {
     typedef typename VT<VEC>::T V;
@@ -363,7 +370,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_update_fused(const __grid_consta
     for (int k = 0; k <= MC; ++k) v[k] = 0.0;
     constexpr int UU1 = U;  // pass-1 elements per trip
     // ROLL: rolling prefetch in passes 1 and 2 (one element per trip; u1_roll / u2_roll)
-    constexpr bool ROLL = OC && MC >= IG_ROLL_MIN && U == 1 && FusedUnroll<MC>::U2 == 1;
+    constexpr bool ROLL = (OC ? MC >= IG_ROLL_MIN : MC >= IG_ROLL_BIG_MIN) && U == 1 && FusedUnroll<MC>::U2 == 1;
     if constexpr (ROLL) {
         U2Trip<MC, 1, V> r1;
         const int nload = pend ? M : deff;
@@ -631,14 +638,14 @@ static int mcb(int M) { return M <= 1 ? 1 : M <= 2 ? 2 : M <= 4 ? 4 : M <= 8 ? 8
         }                                                                                           \
     } while (0)
 
-// Rolling form kernel for M = 17..32 below 2^24 DOFs (A/B, profiles/r3_roll_ab.md: N = 1e6
-// QR(30) 335.5 -> 330.8, 1e7 QR(30) 3024 -> 2987 us/step; neutral at M = 16 and 0.8 us slower at
-// 3e5 QR(12), so the M <= 16 buckets keep the unrolled form).  -DIG_FORM_RF=0 turns it off.
+// Rolling form kernel for M = 17..32 at every N (A/B, profiles/r3_roll_ab.md: N = 1e6 QR(30)
+// 335.5 -> 330.8, 1e7 QR(30) 3024 -> 2987 us/step; neutral at M = 16 and 0.8 us slower at 3e5
+// QR(12), so the M <= 16 buckets keep the unrolled form).  -DIG_FORM_RF=0 turns it off.
 #ifndef IG_FORM_RF
 #define IG_FORM_RF 1
 #endif
 cudaError_t launch_form_fused(const ProjArgs &a, int vec, int nsm, cudaStream_t s) {
-    if (IG_FORM_RF && vec == 2 && mcb(a.M) == 32 && a.N < (int64_t(1) << 24))
+    if (IG_FORM_RF && vec == 2 && mcb(a.M) == 32)
         return coop_launch(k_form_fused<32, 2, true>, a, nsm, s);
     IG_FUSED_DISPATCH(k_form_fused, a, vec, nsm, s);
 }
