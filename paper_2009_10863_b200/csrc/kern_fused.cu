@@ -58,7 +58,7 @@ constexpr int BLK2 = PS * MAXB;
 // form kernel: N = 2e7 QR(17) 3956 -> 3710, QR(30) 5988 -> 5896; 2^27 QR(24) 33564 -> 32948,
 // QR(30) 40394 -> 39937 us/step.
 #ifndef IG_ROLL_BIG_MIN
-#define IG_ROLL_BIG_MIN 32
+#define IG_ROLL_BIG_MIN 24
 #endif
 // Smallest bucket whose one-copy update kernel runs pass 3 with rolling register sets (u3_roll;
 // buckets whose B~ and X~ columns fit in registers together, i.e. MC = 16; bitwise-identical;
@@ -616,7 +616,14 @@ template <class K> static cudaError_t coop_launch(K kern, const ProjArgs &a, int
     return launch_ex(kern, grid, s, a.coop != 0, a);
 }
 
-static int mcb(int M) { return M <= 1 ? 1 : M <= 2 ? 2 : M <= 4 ? 4 : M <= 8 ? 8 : M <= 16 ? 16 : 32; }
+// History-size buckets of the fused kernels (M = 17..24 has its own bucket: with the 32-column
+// code, M = 17 ran at 0.92 of the copy roofline at 2e7 DOFs -- issue-bound on padded columns).
+#ifndef IG_MC24
+#define IG_MC24 1
+#endif
+static int mcb(int M) {
+    return M <= 1 ? 1 : M <= 2 ? 2 : M <= 4 ? 4 : M <= 8 ? 8 : M <= 16 ? 16 : (IG_MC24 && M <= 24) ? 24 : 32;
+}
 
 #define IG_FUSED_DISPATCH(KERNEL, ARGS, VEC_IN, NSM, STREAM)                                        \
     do {                                                                                            \
@@ -633,6 +640,8 @@ static int mcb(int M) { return M <= 1 ? 1 : M <= 2 ? 2 : M <= 4 ? 4 : M <= 8 ? 8
                           : coop_launch(KERNEL<8, 1>, ARGS, NSM, STREAM);                           \
         case 16: return v2 ? coop_launch(KERNEL<16, 2>, ARGS, NSM, STREAM)                          \
                            : coop_launch(KERNEL<16, 1>, ARGS, NSM, STREAM);                         \
+        case 24: return v2 ? coop_launch(KERNEL<24, 2>, ARGS, NSM, STREAM)                          \
+                           : coop_launch(KERNEL<24, 1>, ARGS, NSM, STREAM);                         \
         default: return v2 ? coop_launch(KERNEL<32, 2>, ARGS, NSM, STREAM)                          \
                            : coop_launch(KERNEL<32, 1>, ARGS, NSM, STREAM);                         \
         }                                                                                           \
@@ -645,15 +654,17 @@ static int mcb(int M) { return M <= 1 ? 1 : M <= 2 ? 2 : M <= 4 ? 4 : M <= 8 ? 8
 #define IG_FORM_RF 1
 #endif
 cudaError_t launch_form_fused(const ProjArgs &a, int vec, int nsm, cudaStream_t s) {
-    if (IG_FORM_RF && vec == 2 && mcb(a.M) == 32)
-        return coop_launch(k_form_fused<32, 2, true>, a, nsm, s);
+    if (IG_FORM_RF && vec == 2 && mcb(a.M) >= 24)
+        return mcb(a.M) == 24 ? coop_launch(k_form_fused<24, 2, true>, a, nsm, s)
+                              : coop_launch(k_form_fused<32, 2, true>, a, nsm, s);
     IG_FUSED_DISPATCH(k_form_fused, a, vec, nsm, s);
 }
 cudaError_t launch_update_fused(const ProjArgs &a, int vec, int nsm, cudaStream_t s) {
     const int mc = mcb(a.M);
     if (vec == 2 && mc >= 16 && a.N < (int64_t(1) << 24))
-        return mc == 16 ? coop_launch(k_update_fused<16, 2, true>, a, nsm, s)
-                        : coop_launch(k_update_fused<32, 2, true>, a, nsm, s);
+        return mc == 16   ? coop_launch(k_update_fused<16, 2, true>, a, nsm, s)
+               : mc == 24 ? coop_launch(k_update_fused<24, 2, true>, a, nsm, s)
+                          : coop_launch(k_update_fused<32, 2, true>, a, nsm, s);
     IG_FUSED_DISPATCH(k_update_fused, a, vec, nsm, s);
 }
 

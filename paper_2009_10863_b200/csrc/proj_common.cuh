@@ -629,11 +629,11 @@ __device__ __forceinline__ void u2_roll(U2Trip<MC, 1, V> &r, const ProjArgs &a, 
     v[MC] = vdot(b1, b1, v[MC]);
 }
 
-// For MC >= 32 (SPLIT) a trip holds only Ax, x and the B~ columns; the X~ columns are loaded
+// For MC > 16 (SPLIT) a trip holds only Ax, x and the B~ columns; the X~ columns are loaded
 // (all at once) after the B~ part is finished, so the two 32-column register sets are never live
 // together and the pass can use 16-byte loads (VEC = 2) within the register file.
 template <int MC, int U, class V> struct U3Trip {  // update pass 3: U strided elements
-    static constexpr bool SPLIT = MC >= 32;
+    static constexpr bool SPLIT = MC > 16;
     V ax[U], xv[U];
     V bc[U][MC];
     V xc[U][SPLIT ? 1 : MC];

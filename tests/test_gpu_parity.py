@@ -77,7 +77,7 @@ SCHEDULES = [pytest.param(True, id="fused"), pytest.param(False, id="split")]
 
 
 @pytest.mark.parametrize("fused", SCHEDULES)
-@pytest.mark.parametrize("M", [1, 2, 3, 5, 8, 12, 16, 30, 32])
+@pytest.mark.parametrize("M", [1, 2, 3, 5, 8, 12, 16, 17, 24, 25, 30, 32])
 def test_proj_qr_open_loop_c1(M, fused):
     # configs[0]: 2D 32x32 5-point Helmholtz, 40 steps
     run_proj_parity(Grid(32, 2), M, 40, fused=fused)
@@ -403,6 +403,31 @@ def test_2p24_open_loop_parity():
     he.close()
 
 
+def test_2p24_open_loop_parity_large_m():
+    """As test_2p24_open_loop_parity for the large-vector kernels of the M = 17..24 bucket
+    (k_form_fused<24, 2, RF>, k_update_fused<24, 2> with rolling passes 1-2 and the split pass 3):
+    QR(20) at 2^24 DOFs through history fill and 3 downdates, every guess vs the oracle."""
+    from paper_2009_10863_b200 import InitialGuess
+
+    g = Grid(256, 3)
+    M, steps = 20, 23
+    op, hp = ProjQR(g.N, M), InitialGuess(g.N, "proj_qr", M)
+    x_prev = np.zeros(g.N)
+    for n in range(steps):
+        b, x, Ax = (t.numpy() for t in manufactured_step(g, n))
+        tb, tx, tA = (torch.from_numpy(v).cuda() for v in (b, x, Ax))
+        x0p = torch.from_numpy(x_prev).cuda()
+        hp.form_guess(tb, x0p)
+        e = _rel(x0p.cpu().numpy(), op.form_guess(b, x_prev))
+        assert e <= TOL, f"step {n}: QR guess {e:.3e}"
+        op.update(x, Ax)
+        hp.update(tx, tA)
+        assert hp.d == op.d
+        x_prev = x
+        del tb, tx, tA, x0p
+    hp.close()
+
+
 # ------------------------------------------------------------------ sparse extrapolation (NEXT row f2)
 @pytest.mark.parametrize("m,M", [(2, 8), (3, 8), (3, 16), (2, 12), (5, 30), (0, 4), (3, 4)])
 def test_sparse_weights_match_exact_cpqr(m, M):
@@ -627,7 +652,7 @@ def test_properties_at_full_size(N, M, p):
 
 # ------------------------------------------------------------------ planner CTA edge grids
 @pytest.mark.parametrize("grid", [1, 2, 3, 37])
-@pytest.mark.parametrize("M", [1, 2, 8, 30])
+@pytest.mark.parametrize("M", [1, 2, 8, 20, 30])
 def test_planner_cta_and_single_cta_grids(grid, M):
     """The last CTA of a QR update grid is the planner (R update + Givens plan); with a
     one-CTA grid the plan runs serially in CTA 0.  Grids of 1, 2 (one streaming CTA + planner),
