@@ -51,7 +51,7 @@ constexpr int BLK2 = PS * MAXB;
 // QR(16) 49.5 -> 48.0, 1e6 QR(12) 137.0 -> 134.0, QR(24) 281.2 -> 275.3, QR(30) 339 -> 336,
 // 3e6 QR(16) 510 -> 505, 1e7 QR(16) 1615 -> 1601 us/step).  -DIG_ROLL_MIN=64 turns it off.
 #ifndef IG_ROLL_MIN
-#define IG_ROLL_MIN 16
+#define IG_ROLL_MIN 12
 #endif
 // The same for the large-vector (two-copy) kernels: the M = 17..32 bucket only (the M = 16
 // kernel's register allocation is fragile); profiles/r3_roll_ab.md, with the rolling
@@ -65,7 +65,7 @@ constexpr int BLK2 = PS * MAXB;
 // profiles/r3_roll_ab.md: N = 1e6 QR(16) 171.9 -> 169.5, QR(12) 133.2 -> 131.8, QR(9) 109.3 ->
 // 108.3 us/step; 1e7 QR(16) 1602 -> 1609).  -DIG_ROLL3_MIN=64 turns it off.
 #ifndef IG_ROLL3_MIN
-#define IG_ROLL3_MIN 16
+#define IG_ROLL3_MIN 12
 #endif
 
 // RF: rolling prefetch in both passes (one element per trip, u1_roll-style: the next element's
@@ -621,8 +621,12 @@ template <class K> static cudaError_t coop_launch(K kern, const ProjArgs &a, int
 #ifndef IG_MC24
 #define IG_MC24 1
 #endif
+#ifndef IG_MC12
+#define IG_MC12 1
+#endif
 static int mcb(int M) {
-    return M <= 1 ? 1 : M <= 2 ? 2 : M <= 4 ? 4 : M <= 8 ? 8 : M <= 16 ? 16 : (IG_MC24 && M <= 24) ? 24 : 32;
+    return M <= 1 ? 1 : M <= 2 ? 2 : M <= 4 ? 4 : M <= 8 ? 8 : (IG_MC12 && M <= 12) ? 12 : M <= 16 ? 16
+         : (IG_MC24 && M <= 24) ? 24 : 32;
 }
 
 #define IG_FUSED_DISPATCH(KERNEL, ARGS, VEC_IN, NSM, STREAM)                                        \
@@ -638,6 +642,8 @@ static int mcb(int M) {
                           : coop_launch(KERNEL<4, 1>, ARGS, NSM, STREAM);                           \
         case 8: return v2 ? coop_launch(KERNEL<8, 2>, ARGS, NSM, STREAM)                            \
                           : coop_launch(KERNEL<8, 1>, ARGS, NSM, STREAM);                           \
+        case 12: return v2 ? coop_launch(KERNEL<12, 2>, ARGS, NSM, STREAM)                          \
+                           : coop_launch(KERNEL<12, 1>, ARGS, NSM, STREAM);                         \
         case 16: return v2 ? coop_launch(KERNEL<16, 2>, ARGS, NSM, STREAM)                          \
                            : coop_launch(KERNEL<16, 1>, ARGS, NSM, STREAM);                         \
         case 24: return v2 ? coop_launch(KERNEL<24, 2>, ARGS, NSM, STREAM)                          \
@@ -661,8 +667,9 @@ cudaError_t launch_form_fused(const ProjArgs &a, int vec, int nsm, cudaStream_t 
 }
 cudaError_t launch_update_fused(const ProjArgs &a, int vec, int nsm, cudaStream_t s) {
     const int mc = mcb(a.M);
-    if (vec == 2 && mc >= 16 && a.N < (int64_t(1) << 24))
-        return mc == 16   ? coop_launch(k_update_fused<16, 2, true>, a, nsm, s)
+    if (vec == 2 && mc >= 12 && a.N < (int64_t(1) << 24))
+        return mc == 12   ? coop_launch(k_update_fused<12, 2, true>, a, nsm, s)
+               : mc == 16 ? coop_launch(k_update_fused<16, 2, true>, a, nsm, s)
                : mc == 24 ? coop_launch(k_update_fused<24, 2, true>, a, nsm, s)
                           : coop_launch(k_update_fused<32, 2, true>, a, nsm, s);
     IG_FUSED_DISPATCH(k_update_fused, a, vec, nsm, s);

@@ -426,7 +426,7 @@ __device__ __forceinline__ void u2_trip(const ProjArgs &a, int64_t i0, int64_t s
 // larger buckets.  Fills `reg` from `smem` when registers are used and returns the pointer type
 // the trip functions index.
 template <int MC> struct Coef {
-    static constexpr bool SMEM = MC >= 16;
+    static constexpr bool SMEM = MC > 8;
     typedef typename std::conditional<SMEM, const volatile double *, const double *>::type P;
     double reg[SMEM ? 1 : MC];
     __device__ __forceinline__ P bind(const double *smem) {
@@ -506,9 +506,9 @@ template <int MC> struct FusedUnroll {
     static constexpr int FORM_P1 = IG_T(P1, MC, (MC == 8 ? 3 : 1));
     static constexpr int FORM_P2 = IG_T(P2, MC, (MC == 8 ? 3 : 1));
     static constexpr int FORM_PF = MC == 8 ? 1 : (MC < 8 ? 2 : 1);
-    // For MC >= 16 the per-column coefficients (c1, c2, Givens c/s) are read from shared memory
+    // For MC > 8 the per-column coefficients (c1, c2, Givens c/s) are read from shared memory
     // at each use instead of living in 4*MC registers, which the column loads need.
-    static constexpr bool SMEM_COEF = MC >= 16;
+    static constexpr bool SMEM_COEF = MC > 8;
 };
 
 // ------------------------------------------------------------------ trip = loads, then arithmetic

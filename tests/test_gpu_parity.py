@@ -77,7 +77,7 @@ SCHEDULES = [pytest.param(True, id="fused"), pytest.param(False, id="split")]
 
 
 @pytest.mark.parametrize("fused", SCHEDULES)
-@pytest.mark.parametrize("M", [1, 2, 3, 5, 8, 12, 16, 17, 24, 25, 30, 32])
+@pytest.mark.parametrize("M", [1, 2, 3, 5, 8, 9, 12, 16, 17, 24, 25, 30, 32])
 def test_proj_qr_open_loop_c1(M, fused):
     # configs[0]: 2D 32x32 5-point Helmholtz, 40 steps
     run_proj_parity(Grid(32, 2), M, 40, fused=fused)
@@ -403,14 +403,16 @@ def test_2p24_open_loop_parity():
     he.close()
 
 
-def test_2p24_open_loop_parity_large_m():
-    """As test_2p24_open_loop_parity for the large-vector kernels of the M = 17..24 bucket
-    (k_form_fused<24, 2, RF>, k_update_fused<24, 2> with rolling passes 1-2 and the split pass 3):
-    QR(20) at 2^24 DOFs through history fill and 3 downdates, every guess vs the oracle."""
+@pytest.mark.parametrize("M", [12, 20])
+def test_2p24_open_loop_parity_large_m(M):
+    """As test_2p24_open_loop_parity for the large-vector kernels of the M = 9..12 and 17..24
+    buckets (k_update_fused<12, 2>; k_form_fused<24, 2, RF>, k_update_fused<24, 2> with rolling
+    passes 1-2 and the split pass 3): QR(M) at 2^24 DOFs through history fill and 3 downdates,
+    every guess vs the oracle."""
     from paper_2009_10863_b200 import InitialGuess
 
     g = Grid(256, 3)
-    M, steps = 20, 23
+    steps = M + 3
     op, hp = ProjQR(g.N, M), InitialGuess(g.N, "proj_qr", M)
     x_prev = np.zeros(g.N)
     for n in range(steps):
@@ -652,7 +654,7 @@ def test_properties_at_full_size(N, M, p):
 
 # ------------------------------------------------------------------ planner CTA edge grids
 @pytest.mark.parametrize("grid", [1, 2, 3, 37])
-@pytest.mark.parametrize("M", [1, 2, 8, 20, 30])
+@pytest.mark.parametrize("M", [1, 2, 8, 12, 20, 30])
 def test_planner_cta_and_single_cta_grids(grid, M):
     """The last CTA of a QR update grid is the planner (R update + Givens plan); with a
     one-CTA grid the plan runs serially in CTA 0.  Grids of 1, 2 (one streaming CTA + planner),
