@@ -8,7 +8,7 @@ from paper_2009_10863_b200 import InitialGuess
 from workloads import Grid, manufactured_step
 
 g = Grid(23, 2)  # N = 529: odd, ragged
-for M in (1, 3, 8, 17, 30):
+for M in (1, 3, 8, 12, 17, 30):
     for method, ora_cls in (("proj_qr", ProjQR), ("proj_classic", ProjClassic)):
         for fused in (True, False):
             ora, ig = ora_cls(g.N, M), InitialGuess(g.N, method, M, fused=fused)
