@@ -51,21 +51,21 @@ constexpr int BLK2 = PS * MAXB;
 // QR(16) 49.5 -> 48.0, 1e6 QR(12) 137.0 -> 134.0, QR(24) 281.2 -> 275.3, QR(30) 339 -> 336,
 // 3e6 QR(16) 510 -> 505, 1e7 QR(16) 1615 -> 1601 us/step).  -DIG_ROLL_MIN=64 turns it off.
 #ifndef IG_ROLL_MIN
-#define IG_ROLL_MIN 12
+#define IG_ROLL_MIN 9
 #endif
 // The same for the large-vector (two-copy) kernels: the M = 17..32 bucket only (the M = 16
 // kernel's register allocation is fragile); profiles/r3_roll_ab.md, with the rolling
 // form kernel: N = 2e7 QR(17) 3956 -> 3710, QR(30) 5988 -> 5896; 2^27 QR(24) 33564 -> 32948,
 // QR(30) 40394 -> 39937 us/step.
 #ifndef IG_ROLL_BIG_MIN
-#define IG_ROLL_BIG_MIN 24
+#define IG_ROLL_BIG_MIN 17
 #endif
 // Smallest bucket whose one-copy update kernel runs pass 3 with rolling register sets (u3_roll;
 // buckets whose B~ and X~ columns fit in registers together, i.e. MC = 16; bitwise-identical;
 // profiles/r3_roll_ab.md: N = 1e6 QR(16) 171.9 -> 169.5, QR(12) 133.2 -> 131.8, QR(9) 109.3 ->
 // 108.3 us/step; 1e7 QR(16) 1602 -> 1609).  -DIG_ROLL3_MIN=64 turns it off.
 #ifndef IG_ROLL3_MIN
-#define IG_ROLL3_MIN 12
+#define IG_ROLL3_MIN 9
 #endif
 
 // RF: rolling prefetch in both passes (one element per trip, u1_roll-style: the next element's
@@ -616,17 +616,18 @@ template <class K> static cudaError_t coop_launch(K kern, const ProjArgs &a, int
     return launch_ex(kern, grid, s, a.coop != 0, a);
 }
 
-// History-size buckets of the fused kernels (M = 17..24 has its own bucket: with the 32-column
-// code, M = 17 ran at 0.92 of the copy roofline at 2e7 DOFs -- issue-bound on padded columns).
-#ifndef IG_MC24
-#define IG_MC24 1
-#endif
-#ifndef IG_MC12
-#define IG_MC12 1
+// History-size buckets of the fused kernels.  Columns beyond M are predicated off but still cost
+// issue slots and registers, and at one CTA of 8 warps per SM the first M of a coarse bucket was
+// issue-bound (2^27 DOFs, buckets 1/2/4/8/12/16/24/32: QR(5) 0.92, QR(9) 0.91, QR(13) 0.95,
+// QR(17) 0.95 of copy; profiles/r3_roll_ab.md).  IG_FINE_BUCKETS=0 restores those buckets.
+#ifndef IG_FINE_BUCKETS
+#define IG_FINE_BUCKETS 1
 #endif
 static int mcb(int M) {
-    return M <= 1 ? 1 : M <= 2 ? 2 : M <= 4 ? 4 : M <= 8 ? 8 : (IG_MC12 && M <= 12) ? 12 : M <= 16 ? 16
-         : (IG_MC24 && M <= 24) ? 24 : 32;
+    if (M <= 4) return M <= 1 ? 1 : M <= 2 ? 2 : 4;
+    if (IG_FINE_BUCKETS) return M <= 6 ? 6 : M <= 8 ? 8 : M <= 10 ? 10 : M <= 12 ? 12 : M <= 14 ? 14 : M <= 16 ? 16
+                              : M <= 20 ? 20 : M <= 24 ? 24 : M <= 28 ? 28 : 32;
+    return M <= 8 ? 8 : M <= 12 ? 12 : M <= 16 ? 16 : M <= 24 ? 24 : 32;
 }
 
 #define IG_FUSED_DISPATCH(KERNEL, ARGS, VEC_IN, NSM, STREAM)                                        \
@@ -640,14 +641,24 @@ static int mcb(int M) {
                           : coop_launch(KERNEL<2, 1>, ARGS, NSM, STREAM);                           \
         case 4: return v2 ? coop_launch(KERNEL<4, 2>, ARGS, NSM, STREAM)                            \
                           : coop_launch(KERNEL<4, 1>, ARGS, NSM, STREAM);                           \
+        case 6: return v2 ? coop_launch(KERNEL<6, 2>, ARGS, NSM, STREAM)                            \
+                          : coop_launch(KERNEL<6, 1>, ARGS, NSM, STREAM);                           \
         case 8: return v2 ? coop_launch(KERNEL<8, 2>, ARGS, NSM, STREAM)                            \
                           : coop_launch(KERNEL<8, 1>, ARGS, NSM, STREAM);                           \
+        case 10: return v2 ? coop_launch(KERNEL<10, 2>, ARGS, NSM, STREAM)                          \
+                           : coop_launch(KERNEL<10, 1>, ARGS, NSM, STREAM);                         \
         case 12: return v2 ? coop_launch(KERNEL<12, 2>, ARGS, NSM, STREAM)                          \
                            : coop_launch(KERNEL<12, 1>, ARGS, NSM, STREAM);                         \
+        case 14: return v2 ? coop_launch(KERNEL<14, 2>, ARGS, NSM, STREAM)                          \
+                           : coop_launch(KERNEL<14, 1>, ARGS, NSM, STREAM);                         \
         case 16: return v2 ? coop_launch(KERNEL<16, 2>, ARGS, NSM, STREAM)                          \
                            : coop_launch(KERNEL<16, 1>, ARGS, NSM, STREAM);                         \
+        case 20: return v2 ? coop_launch(KERNEL<20, 2>, ARGS, NSM, STREAM)                          \
+                           : coop_launch(KERNEL<20, 1>, ARGS, NSM, STREAM);                         \
         case 24: return v2 ? coop_launch(KERNEL<24, 2>, ARGS, NSM, STREAM)                          \
                            : coop_launch(KERNEL<24, 1>, ARGS, NSM, STREAM);                         \
+        case 28: return v2 ? coop_launch(KERNEL<28, 2>, ARGS, NSM, STREAM)                          \
+                           : coop_launch(KERNEL<28, 1>, ARGS, NSM, STREAM);                         \
         default: return v2 ? coop_launch(KERNEL<32, 2>, ARGS, NSM, STREAM)                          \
                            : coop_launch(KERNEL<32, 1>, ARGS, NSM, STREAM);                         \
         }                                                                                           \
@@ -660,18 +671,26 @@ static int mcb(int M) {
 #define IG_FORM_RF 1
 #endif
 cudaError_t launch_form_fused(const ProjArgs &a, int vec, int nsm, cudaStream_t s) {
-    if (IG_FORM_RF && vec == 2 && mcb(a.M) >= 24)
-        return mcb(a.M) == 24 ? coop_launch(k_form_fused<24, 2, true>, a, nsm, s)
-                              : coop_launch(k_form_fused<32, 2, true>, a, nsm, s);
+    if (IG_FORM_RF && vec == 2 && mcb(a.M) > 16) switch (mcb(a.M)) {
+        case 20: return coop_launch(k_form_fused<20, 2, true>, a, nsm, s);
+        case 24: return coop_launch(k_form_fused<24, 2, true>, a, nsm, s);
+        case 28: return coop_launch(k_form_fused<28, 2, true>, a, nsm, s);
+        default: return coop_launch(k_form_fused<32, 2, true>, a, nsm, s);
+        }
     IG_FUSED_DISPATCH(k_form_fused, a, vec, nsm, s);
 }
 cudaError_t launch_update_fused(const ProjArgs &a, int vec, int nsm, cudaStream_t s) {
     const int mc = mcb(a.M);
-    if (vec == 2 && mc >= 12 && a.N < (int64_t(1) << 24))
-        return mc == 12   ? coop_launch(k_update_fused<12, 2, true>, a, nsm, s)
-               : mc == 16 ? coop_launch(k_update_fused<16, 2, true>, a, nsm, s)
-               : mc == 24 ? coop_launch(k_update_fused<24, 2, true>, a, nsm, s)
-                          : coop_launch(k_update_fused<32, 2, true>, a, nsm, s);
+    if (vec == 2 && mc > 8 && a.N < (int64_t(1) << 24)) switch (mc) {
+        case 10: return coop_launch(k_update_fused<10, 2, true>, a, nsm, s);
+        case 12: return coop_launch(k_update_fused<12, 2, true>, a, nsm, s);
+        case 14: return coop_launch(k_update_fused<14, 2, true>, a, nsm, s);
+        case 16: return coop_launch(k_update_fused<16, 2, true>, a, nsm, s);
+        case 20: return coop_launch(k_update_fused<20, 2, true>, a, nsm, s);
+        case 24: return coop_launch(k_update_fused<24, 2, true>, a, nsm, s);
+        case 28: return coop_launch(k_update_fused<28, 2, true>, a, nsm, s);
+        default: return coop_launch(k_update_fused<32, 2, true>, a, nsm, s);
+        }
     IG_FUSED_DISPATCH(k_update_fused, a, vec, nsm, s);
 }
 

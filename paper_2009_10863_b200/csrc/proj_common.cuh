@@ -503,9 +503,9 @@ template <int MC> struct FusedUnroll {
     static constexpr int U = IG_T(U, MC, (MC <= 8 ? 2 : 1));
     static constexpr int U3 = IG_T(U3, MC, 1);
     static constexpr int U2 = IG_T(U2, MC, (MC <= 8 ? 2 : 1));
-    static constexpr int FORM_P1 = IG_T(P1, MC, (MC == 8 ? 3 : 1));
-    static constexpr int FORM_P2 = IG_T(P2, MC, (MC == 8 ? 3 : 1));
-    static constexpr int FORM_PF = MC == 8 ? 1 : (MC < 8 ? 2 : 1);
+    static constexpr int FORM_P1 = IG_T(P1, MC, ((MC > 4 && MC <= 8) ? 3 : 1));
+    static constexpr int FORM_P2 = IG_T(P2, MC, ((MC > 4 && MC <= 8) ? 3 : 1));
+    static constexpr int FORM_PF = (MC > 4 && MC <= 8) ? 1 : (MC < 8 ? 2 : 1);
     // For MC > 8 the per-column coefficients (c1, c2, Givens c/s) are read from shared memory
     // at each use instead of living in 4*MC registers, which the column loads need.
     static constexpr bool SMEM_COEF = MC > 8;

@@ -77,7 +77,7 @@ SCHEDULES = [pytest.param(True, id="fused"), pytest.param(False, id="split")]
 
 
 @pytest.mark.parametrize("fused", SCHEDULES)
-@pytest.mark.parametrize("M", [1, 2, 3, 5, 8, 9, 12, 16, 17, 24, 25, 30, 32])
+@pytest.mark.parametrize("M", [1, 2, 3, 5, 6, 8, 9, 10, 12, 13, 14, 16, 17, 20, 24, 25, 28, 30, 32])
 def test_proj_qr_open_loop_c1(M, fused):
     # configs[0]: 2D 32x32 5-point Helmholtz, 40 steps
     run_proj_parity(Grid(32, 2), M, 40, fused=fused)
