@@ -95,6 +95,15 @@ def test_proj_qr_ragged_sizes(n, dim, fused):
     run_proj_parity(Grid(n, dim), 8, 14, dt=1e-2, fused=fused)
 
 
+@pytest.mark.parametrize("M", [6, 10, 12, 14, 16, 20, 28, 32])
+def test_proj_qr_buckets_multi_trip_odd_n(M):
+    """Every history bucket of the fused kernels (rolling passes, one-copy pass 3, split pass 3,
+    rolling form) on an odd, multi-trip vector: 61^3 = 226,981 DOFs (three grid-stride trips per
+    thread with a ragged last one, plus the odd scalar tail), through fill, downdates and the
+    dynamic pass-3 claims."""
+    run_proj_parity(Grid(61, 3), M, M + 4, dt=1e-2)
+
+
 @pytest.mark.parametrize("fused", SCHEDULES)
 def test_proj_qr_misaligned_vectors_take_scalar_path(fused):
     run_proj_parity(Grid(33, 2), 4, 12, misalign=True, fused=fused)
