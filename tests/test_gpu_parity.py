@@ -105,8 +105,9 @@ def test_proj_qr_buckets_multi_trip_odd_n(M):
 
 
 @pytest.mark.parametrize("fused", SCHEDULES)
-def test_proj_qr_misaligned_vectors_take_scalar_path(fused):
-    run_proj_parity(Grid(33, 2), 4, 12, misalign=True, fused=fused)
+@pytest.mark.parametrize("M", [4, 6, 10, 14, 20, 28])
+def test_proj_qr_misaligned_vectors_take_scalar_path(M, fused):
+    run_proj_parity(Grid(33, 2), M, M + 6, misalign=True, fused=fused)
 
 
 @pytest.mark.parametrize("fused", SCHEDULES)
