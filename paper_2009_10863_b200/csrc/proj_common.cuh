@@ -499,6 +499,12 @@ template <int MC> struct Coef {
 #ifndef IG_T_P2_4
 #define IG_T_P2_4 6
 #endif
+// Buckets above IG_SMEM_COEF_MIN read the per-column coefficients from shared memory; up to it they
+// live in registers (A/B, profiles/r3_roll_ab.md: registers for MC = 10/12 2^27 QR(9) 0.934 ->
+// 0.950, QR(12) 0.962 -> 0.988, bitwise-identical; for MC = 14 they spill and run 2-3 % slower).
+#ifndef IG_SMEM_COEF_MIN
+#define IG_SMEM_COEF_MIN 12
+#endif
 template <int MC> struct FusedUnroll {
     static constexpr int U = IG_T(U, MC, (MC <= 8 ? 2 : 1));
     static constexpr int U3 = IG_T(U3, MC, 1);
@@ -506,9 +512,9 @@ template <int MC> struct FusedUnroll {
     static constexpr int FORM_P1 = IG_T(P1, MC, ((MC > 4 && MC <= 8) ? 3 : 1));
     static constexpr int FORM_P2 = IG_T(P2, MC, ((MC > 4 && MC <= 8) ? 3 : 1));
     static constexpr int FORM_PF = (MC > 4 && MC <= 8) ? 1 : (MC < 8 ? 2 : 1);
-    // For MC > 8 the per-column coefficients (c1, c2, Givens c/s) are read from shared memory
+    // For MC > IG_SMEM_COEF_MIN the per-column coefficients (c1, c2, Givens c/s) are read from shared memory
     // at each use instead of living in 4*MC registers, which the column loads need.
-    static constexpr bool SMEM_COEF = MC > 8;
+    static constexpr bool SMEM_COEF = MC > IG_SMEM_COEF_MIN;
 };
 
 // ------------------------------------------------------------------ trip = loads, then arithmetic
