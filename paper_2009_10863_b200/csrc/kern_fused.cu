@@ -625,7 +625,10 @@ template <class K> static cudaError_t coop_launch(K kern, const ProjArgs &a, int
 #endif
 static int mcb(int M) {
     if (M <= 4) return M <= 1 ? 1 : M <= 2 ? 2 : 4;
-    if (IG_FINE_BUCKETS) return M <= 6 ? 6 : M <= 8 ? 8 : M <= 10 ? 10 : M <= 12 ? 12 : M <= 14 ? 14 : M <= 16 ? 16
+#ifndef IG_MC5
+#define IG_MC5 1
+#endif
+    if (IG_FINE_BUCKETS) return (IG_MC5 && M == 5) ? 5 : M <= 6 ? 6 : M <= 8 ? 8 : M <= 10 ? 10 : M <= 12 ? 12 : M <= 14 ? 14 : M <= 16 ? 16
                               : M <= 20 ? 20 : M <= 24 ? 24 : M <= 28 ? 28 : 32;
     return M <= 8 ? 8 : M <= 12 ? 12 : M <= 16 ? 16 : M <= 24 ? 24 : 32;
 }
@@ -641,6 +644,8 @@ static int mcb(int M) {
                           : coop_launch(KERNEL<2, 1>, ARGS, NSM, STREAM);                           \
         case 4: return v2 ? coop_launch(KERNEL<4, 2>, ARGS, NSM, STREAM)                            \
                           : coop_launch(KERNEL<4, 1>, ARGS, NSM, STREAM);                           \
+        case 5: return v2 ? coop_launch(KERNEL<5, 2>, ARGS, NSM, STREAM)                            \
+                          : coop_launch(KERNEL<5, 1>, ARGS, NSM, STREAM);                           \
         case 6: return v2 ? coop_launch(KERNEL<6, 2>, ARGS, NSM, STREAM)                            \
                           : coop_launch(KERNEL<6, 1>, ARGS, NSM, STREAM);                           \
         case 8: return v2 ? coop_launch(KERNEL<8, 2>, ARGS, NSM, STREAM)                            \

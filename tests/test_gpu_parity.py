@@ -95,7 +95,7 @@ def test_proj_qr_ragged_sizes(n, dim, fused):
     run_proj_parity(Grid(n, dim), 8, 14, dt=1e-2, fused=fused)
 
 
-@pytest.mark.parametrize("M", [6, 10, 12, 14, 16, 20, 28, 32])
+@pytest.mark.parametrize("M", [5, 6, 10, 12, 14, 16, 20, 28, 32])
 def test_proj_qr_buckets_multi_trip_odd_n(M):
     """Every history bucket of the fused kernels (rolling passes, one-copy pass 3, split pass 3,
     rolling form) on an odd, multi-trip vector: 61^3 = 226,981 DOFs (three grid-stride trips per
@@ -105,7 +105,7 @@ def test_proj_qr_buckets_multi_trip_odd_n(M):
 
 
 @pytest.mark.parametrize("fused", SCHEDULES)
-@pytest.mark.parametrize("M", [4, 6, 10, 14, 20, 28])
+@pytest.mark.parametrize("M", [4, 5, 6, 10, 14, 20, 28])
 def test_proj_qr_misaligned_vectors_take_scalar_path(M, fused):
     run_proj_parity(Grid(33, 2), M, M + 6, misalign=True, fused=fused)
 
