@@ -13,6 +13,9 @@
 //                    --> CTA 0 writes the control block (no exit barrier); the planner CTA
 //                    (the last one, QR) computes R and the next downdate's Givens plan
 //                    alongside (its prefix during passes 1-2, its suffix after barrier 2)
+// Every kernel is instantiated per history bucket MC (mcb(): 1, 2, 4, 5, 6, 8, 10, ..., 32); the
+// large buckets use the rolling prefetch (u1_roll / u2_roll / u3_roll, RF form) and, below 2^24
+// DOFs, the one-copy pass-3 loop (OC) -- separate instantiations chosen by the launchers.
 // Barrier and claim counters are double-buffered by a launch epoch in the control block.  The
 // element arithmetic is the same device code as the one-kernel-per-pass path (proj_common.cuh),
 // which stays in use when partial sums cross ranks through an all-gather (ig_attach_comm); with
