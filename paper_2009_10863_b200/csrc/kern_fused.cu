@@ -63,12 +63,16 @@ constexpr int BLK2 = PS * MAXB;
 #ifndef IG_ROLL_BIG_MIN
 #define IG_ROLL_BIG_MIN 17
 #endif
-// Smallest bucket whose one-copy update kernel runs pass 3 with rolling register sets (u3_roll;
-// buckets whose B~ and X~ columns fit in registers together, i.e. MC = 16; bitwise-identical;
-// profiles/r3_roll_ab.md: N = 1e6 QR(16) 171.9 -> 169.5, QR(12) 133.2 -> 131.8, QR(9) 109.3 ->
-// 108.3 us/step; 1e7 QR(16) 1602 -> 1609).  -DIG_ROLL3_MIN=64 turns it off.
+// Buckets [IG_ROLL3_MIN, IG_ROLL3_MAX] of the one-copy update kernel run pass 3 with rolling
+// register sets (u3_roll; the buckets whose B~ and X~ columns fit in registers together;
+// bitwise-identical; profiles/r3_roll_ab.md: N = 1e6 QR(16) 171.9 -> 169.5, QR(12) 133.2 ->
+// 131.8, QR(9) 109.3 -> 108.3 us/step; 1e7 QR(16) 1602 -> 1609; MC = 20 spills and was slower
+// at 3e6-1e7).  -DIG_ROLL3_MIN=64 turns it off.
 #ifndef IG_ROLL3_MIN
 #define IG_ROLL3_MIN 9
+#endif
+#ifndef IG_ROLL3_MAX
+#define IG_ROLL3_MAX 16
 #endif
 
 // RF: rolling prefetch in both passes (one element per trip, u1_roll-style: the next element's
@@ -429,7 +433,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_update_fused(const __grid_consta
         }
     }
     // first trip of pass 3, in flight across barrier 2 (ROLL3: the B~ part of the first element)
-    constexpr bool ROLL3 = OC && MC >= IG_ROLL3_MIN && U3 == 1 && !U3Trip<MC, 1, V>::SPLIT;
+    constexpr bool ROLL3 = OC && MC >= IG_ROLL3_MIN && MC <= IG_ROLL3_MAX && U3 == 1;
     U3Trip<MC, U3, V> pre3;
     R3<MC, V> r3;
     if constexpr (ROLL3)
